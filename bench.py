@@ -1,0 +1,390 @@
+"""Benchmark of the row-wise top-k hot path on B200 (BASELINE.json configs[1]).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+                    [--workload c2|reddit|c5|sweep] [--mode exact|early]
+
+One step = one pass of the hot path (one fused kernel launch) over the whole
+synthetic batch: N = 2^20 rows x M = 256 fp32 (i.i.d. N(0,1), the reference
+generator datagen.py:49-52 run on the device), k = 32, exact mode (the
+headline) -- early stop max_iter=4 is measured in the same run and reported
+under "modes".  Inputs (1 GiB) exceed the 126 MB L2, so no flush is needed.
+
+value     rows/s of the whole job (all ranks), input resident in HBM, timed
+          with CUDA events on the launching stream, max over ranks.
+e2e       the same metric through the public API batch_topk() with pinned
+          host buffers: H2D of the matrix + kernel + D2H of values/indices.
+roofline  HBM-bound: algorithmic bytes N*(4M + 8k) per launch / mean launch
+          time vs MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline  the oracle port (oracle/rtk_oracle.c, a C restatement of the
+          reference kernels) on all host cores, rank 0, N=1 only.
+
+Multi-GPU (torchrun): rows are sharded with no collective; each rank runs the
+per-GPU workload on its own rows (weak scaling).
+--impl reference: the reference CPU implementation of the path (its C port,
+since the reference is Python+numba and cannot travel to the GPU box) on the
+host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (N rows per GPU, M, k)
+    "c2": (1 << 20, 256, 32),
+    "reddit": (232965, 256, 32),
+    "c5": (1 << 24, 512, 64),  # per-GPU share is N/G under --strong
+}
+METRIC = "rows/sec and HBM GB/s of row-wise top-k (N×M fp32, k) vs torch.topk"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    p.add_argument("--mode", default="exact", choices=["exact", "early"])
+    p.add_argument("--max-iter", type=int, default=4)
+    p.add_argument("--strong", action="store_true", help="shard a fixed global N across ranks")
+    p.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--seed", type=int, default=0)
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(workload, mode):
+    """dram bytes per launch from the committed ncu --set full capture, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(f"{workload}:{mode}")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML polling thread (~2 ms) for SM clocks and throttle reasons."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._active = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+
+    _NAMES = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def _run(self):
+        while not self._stop.is_set():
+            if self._active.is_set():
+                try:
+                    self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                    r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                    for bit, name in self._NAMES.items():
+                        if r & bit and bit != 0x1:
+                            self.reasons.add(name)
+                except Exception:
+                    pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def start(self):
+        self._active.set()
+
+    def stop(self):
+        self._active.clear()
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_setup(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local) if torch.cuda.is_available() else None
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    return rank, world, local
+
+
+def reduce_max(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def make_input(n, m, seed, rank, device):
+    """N(0,1) fp32 on the device (torch Philox, per-rank seed)."""
+    import torch
+
+    g = torch.Generator(device=device).manual_seed(seed * 1000003 + rank)
+    return torch.randn((n, m), device=device, dtype=torch.float32, generator=g)
+
+
+def time_launches(fn, steps, warmup, world, stream, sampler=None):
+    """W untimed steps, then K steps between events on `stream`; returns mean ms per step (max over ranks)."""
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    if sampler:
+        sampler.start()
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.stop()
+    barrier(world)
+    ms = e0.elapsed_time(e1) / steps
+    return reduce_max(ms, world)
+
+
+def cpu_oracle_rate(x_np, k, mode, max_iter, threads, reps=3, budget_s=30.0):
+    """Rows/s of the oracle port on the host (median of reps)."""
+    import oracle
+
+    oracle.build()
+    t0 = time.perf_counter()
+    oracle.ref_batch(x_np, k, mode, max_iter=max_iter, threads=threads)  # warm-up pass
+    first = time.perf_counter() - t0
+    reps = max(1, min(reps, int(budget_s / max(first, 1e-3))))
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        oracle.ref_batch(x_np, k, mode, max_iter=max_iter, threads=threads)
+        ts.append(time.perf_counter() - t0)
+    return x_np.shape[0] / statistics.median(ts), reps
+
+
+def run_reference(args):
+    """--impl reference: the reference CPU path (C port) on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    import oracle
+
+    oracle.build()
+    n, m, k = WORKLOADS[args.workload]
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    # one step = a bounded row sample of the workload, sized so the whole run stays ~2 min
+    probe_rows = min(n, 1 << 16)
+    x = np.random.default_rng(args.seed).standard_normal((probe_rows, m), dtype=np.float32)
+    t0 = time.perf_counter()
+    oracle.ref_batch(x, k, args.mode, max_iter=args.max_iter, threads=threads)
+    per_row = (time.perf_counter() - t0) / probe_rows
+    total_steps = args.steps + args.warmup
+    rows = int(min(n, max(4096, 120.0 / max(total_steps, 1) / max(per_row, 1e-9))))
+    x = np.random.default_rng(args.seed).standard_normal((rows, m), dtype=np.float32)
+    for _ in range(args.warmup):
+        oracle.ref_batch(x, k, args.mode, max_iter=args.max_iter, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.ref_batch(x, k, args.mode, max_iter=args.max_iter, threads=threads)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = rows / dt
+    sample = f"{rows} of {n} rows x {m} fp32 N(0,1), k={k}, {args.mode} per step"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic N(0,1) (numpy default_rng)",
+        "config": {"workload": args.workload, "N": n, "M": m, "k": k, "mode": args.mode,
+                   "max_iter": args.max_iter if args.mode == "early" else None},
+        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gb_per_s": value * (4 * m + 8 * k) / 1e9,
+        "note": "reference = oracle/rtk_oracle.c, a C restatement of rowtopk/_kernels.py on all host threads "
+                "(the Python/numba reference cannot travel to the GPU box)",
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+
+    import paper_2409_00822_b200 as rtk
+    from paper_2409_00822_b200 import _build, _native
+
+    _build.build()
+    rank, world, local = dist_setup(args)
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    n_cfg, m, k = WORKLOADS[args.workload]
+    n = n_cfg // world if args.strong else n_cfg
+    if args.strong:
+        from paper_2409_00822_b200.shard import shard_range
+
+        a, b = shard_range(n_cfg, rank, world)
+        n = b - a
+    stream = torch.cuda.current_stream(dev)
+    x = make_input(n, m, args.seed, rank, dev)
+    dm = rtk.batch._DeviceMatrix(x)
+    searches = {"exact": rtk.SearchConfig.exact(), "early": rtk.SearchConfig.early_stop(args.max_iter)}
+    nan_word = dm._new_nan_word()
+    outs = {md: dm.launch_topk(k, s, False, nan_word=nan_word) for md, s in searches.items()}
+    torch.cuda.synchronize()
+    assert int(nan_word.item()) == -1
+
+    peak, peak_src = peaks()
+    bytes_per_launch = n * (4 * m + 8 * k)
+    results = {}
+    with ClockSampler(local) as sampler:
+        for md, s in searches.items():
+            o = outs[md]
+
+            def step(o=o, s=s):
+                dm.launch_topk(k, s, False, outputs=o, nan_word=nan_word)
+
+            smp = sampler if md == args.mode else None
+            ms = time_launches(step, args.steps, args.warmup, world, stream, smp)
+            results[md] = {"ms_per_step": ms, "rows_per_s": world * n / (ms * 1e-3),
+                           "gb_per_s_per_gpu": bytes_per_launch / (ms * 1e-3) / 1e9}
+        clocks = sampler.summary()
+
+    # torch.topk on the same device-resident input (the paper's comparison point)
+    tk = {}
+    for sorted_ in (True, False):
+        ms = time_launches(lambda: torch.topk(x, k, dim=1, sorted=sorted_), max(5, args.steps // 10),
+                           3, world, stream)
+        tk["sorted" if sorted_ else "unsorted"] = {"ms_per_step": ms, "rows_per_s": world * n / (ms * 1e-3)}
+    head = results[args.mode]
+    speedup_vs_torch = tk["sorted"]["ms_per_step"] / head["ms_per_step"]
+
+    # e2e through the public API with pinned host buffers (H2D + kernel + D2H each step)
+    e2e = None
+    if not args.no_e2e:
+        xh = x.cpu().pin_memory()
+        cfg = rtk.BatchConfig(k=k, search=searches[args.mode])
+        e2e_steps = max(3, min(args.steps, 10))
+        for _ in range(2):
+            rtk.batch_topk(xh, cfg)
+        torch.cuda.synchronize()
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            res = rtk.batch_topk(xh, cfg)
+        torch.cuda.synchronize()
+        dt = reduce_max((time.perf_counter() - t0) / e2e_steps, world)
+        e2e = {"value": world * n / dt, "unit": "rows/s", "h2d_bytes_per_step": int(xh.numel() * 4),
+               "d2h_bytes_per_step": int(res.values.nbytes + res.indices.nbytes + 4), "steps": e2e_steps,
+               "ms_per_step": dt * 1e3}
+        del xh
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+        rows = min(n, 1 << 18)
+        x_np = x[:rows].cpu().numpy()
+        rate, reps = cpu_oracle_rate(x_np, k, args.mode, args.max_iter, threads)
+        cpu = {"value": rate, "unit": "rows/s", "cores": threads, "kind": "port",
+               "sample": f"first {rows} rows of the workload (M={m}, k={k}, {args.mode}), median of {reps}"}
+
+    achieved = bytes_per_launch / (head["ms_per_step"] * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": head["rows_per_s"], "unit": "rows/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
+        "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic N(0,1) fp32 generated on device (torch Philox), per-rank seed",
+        "config": {"workload": args.workload, "N_per_gpu": n, "M": m, "k": k, "mode": args.mode,
+                   "max_iter": args.max_iter if args.mode == "early" else None, "parallelism": f"rows/{world}",
+                   "l2": "input > L2 (no flush needed)", "model": None, "global_batch": world * n, "seq_len": m},
+        "gb_per_s": world * achieved,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": ncu_traffic(args.workload, args.mode), "peak_source": peak_src,
+                     "bytes_per_launch": bytes_per_launch},
+        "modes": results,
+        "torch_topk": tk, "speedup_vs_torch_topk_sorted": speedup_vs_torch,
+        "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": args.steps,
+        "library": _native.library_path(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

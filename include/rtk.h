@@ -1,0 +1,118 @@
+/*
+ * rtk.h -- C ABI of the B200-native row-wise top-k library (librtk.so).
+ *
+ * Drop-in boundary for the reference's operator layer
+ *   /root/reference/pkg/src/rowtopk/_kernels.py
+ * whose chunk kernels the reference batch engine calls per row chunk
+ * (batch.py:125-128 and batch.py:133-136).  Conventions mirror that operator:
+ *   - the caller allocates every output (batch.py:114-117); the library never
+ *     allocates, frees or synchronises;
+ *   - the caller validates arguments first (batch.py:107-112); the library
+ *     re-checks sizes and returns RTK_EINVAL instead of raising;
+ *   - calls are reentrant; concurrent calls must write disjoint outputs
+ *     (batch.py:3-5).
+ * Differences forced by the device boundary:
+ *   - all array pointers are DEVICE pointers (cudaMalloc / torch CUDA
+ *     storage), work is enqueued asynchronously on `stream` (a cudaStream_t,
+ *     NULL = legacy default stream);
+ *   - NaN rejection (batch.py:37-39) is fused into the kernels: when
+ *     `nan_first_row` is non-NULL it must point to one device uint32; the call
+ *     resets it to 0xFFFFFFFF and the kernels atomically lower it to the index
+ *     of the first row holding a NaN.  The caller reads it after the stream
+ *     completes and raises NaNInputError (rows with NaN get unspecified output).
+ *
+ * Row layout: x is row-major, row r starts at x + r*ldx (ldx >= m).  Outputs
+ * row r start at vals + r*ldo / idx + r*ldo (ldo >= k).  Exactly k values and
+ * k int32 indices are written per row, indices ascending, values bit copies
+ * of x (_kernels.py:106-146).  iters (int32) / reasons (int8, ExitReason codes
+ * 1..5, _kernels.py:19-23) are per-row traces and may be NULL (trace
+ * collection off, BatchConfig.collect_traces=False, batch.py:58).
+ *
+ * Return value: RTK_OK, RTK_EINVAL (bad sizes, k not in [1, m], NULL
+ * required pointer), or RTK_ECUDA (launch failure); rtk_last_error() then
+ * returns a thread-local message.
+ */
+#ifndef RTK_H_
+#define RTK_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define RTK_API __attribute__((visibility("default")))
+#else
+#define RTK_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RTK_OK 0
+#define RTK_EINVAL 1
+#define RTK_ECUDA 2
+
+#define RTK_EXIT_COUNT_EQUALS_K 1
+#define RTK_EXIT_INTERVAL_BELOW_EPSILON 2
+#define RTK_EXIT_MAX_ITER_REACHED 3
+#define RTK_EXIT_HARD_CAP_REACHED 4
+#define RTK_EXIT_DEGENERATE_ROW 5
+
+/* Exact mode (Algorithm 1 + select_exact).  Replaces
+ *   _kernels.exact_topk_chunk(data, k, eps_rel, hard_cap,
+ *                             out_vals, out_idx, out_iters, out_reasons)
+ *   (/root/reference/pkg/src/rowtopk/_kernels.py:165-186)
+ * eps_rel >= 0 (SearchConfig.epsilon_rel), hard_cap >= 1 (select.py:36). */
+RTK_API int rtk_rowtopk_exact_f32(const float *x, int64_t n, int64_t m, int64_t ldx, int32_t k,
+                          double eps_rel, int32_t hard_cap, float *vals, int32_t *idx,
+                          int64_t ldo, int32_t *iters, int8_t *reasons,
+                          uint32_t *nan_first_row, void *stream);
+
+/* Early-stop mode (Algorithm 2 + first-k selection).  Replaces
+ *   _kernels.early_topk_chunk(data, k, max_iter,
+ *                             out_vals, out_idx, out_iters, out_reasons)
+ *   (/root/reference/pkg/src/rowtopk/_kernels.py:189-214)
+ * max_iter >= 1 (SearchConfig.max_iter, select.py:37). */
+RTK_API int rtk_rowtopk_early_f32(const float *x, int64_t n, int64_t m, int64_t ldx, int32_t k,
+                          int32_t max_iter, float *vals, int32_t *idx, int64_t ldo,
+                          int32_t *iters, int8_t *reasons, uint32_t *nan_first_row,
+                          void *stream);
+
+/* Exit statistics only, no selection.  Replaces
+ *   _kernels.exact_trace_chunk(data, k, eps_rel, hard_cap, out_iters, out_reasons)
+ *   (/root/reference/pkg/src/rowtopk/_kernels.py:217-231)
+ * iters and reasons are required here. */
+RTK_API int rtk_exact_trace_f32(const float *x, int64_t n, int64_t m, int64_t ldx, int32_t k,
+                        double eps_rel, int32_t hard_cap, int32_t *iters, int8_t *reasons,
+                        uint32_t *nan_first_row, void *stream);
+
+/* NaN scan only: the as_matrix validation pass (batch.py:37-39), used when
+ * the caller must report NaN before a k-range error (batch.py:107-111). */
+RTK_API int rtk_nan_scan_f32(const float *x, int64_t n, int64_t m, int64_t ldx, uint32_t *nan_first_row,
+                     void *stream);
+
+/* Per-row min/max (_kernels.row_min_max, _kernels.py:26-36) and inclusive
+ * count (_kernels.count_ge, _kernels.py:39-45) as batched device ops, backing
+ * the single-row helpers select.min_max / select.count_ge (select.py:116-129).
+ * thres has one float per row; counts are int32. */
+RTK_API int rtk_row_min_max_f32(const float *x, int64_t n, int64_t m, int64_t ldx, float *mins,
+                        float *maxs, void *stream);
+RTK_API int rtk_count_ge_f32(const float *x, int64_t n, int64_t m, int64_t ldx, const float *thres,
+                     int32_t *counts, void *stream);
+
+/* Thread-local description of the last non-OK return. */
+RTK_API const char *rtk_last_error(void);
+
+/* Library ABI version (major*10000 + minor*100 + patch). */
+RTK_API int rtk_version(void);
+
+/* Device-side tuning knobs the host wrapper may report: the warps per CTA and
+ * CTAs per SM the persistent kernels launch with for (m, k, mode); mode 0 =
+ * exact, 1 = early stop, 2 = trace.  Returns RTK_OK or RTK_EINVAL. */
+RTK_API int rtk_launch_shape(int64_t m, int32_t k, int32_t mode, int32_t *warps_per_cta,
+                     int32_t *ctas_per_sm, int32_t *rows_per_warp);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RTK_H_ */

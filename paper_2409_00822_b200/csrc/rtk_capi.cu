@@ -1,0 +1,275 @@
+// rtk_capi.cu -- extern "C" entry points of librtk.so (declared in include/rtk.h).
+//
+// Host-side dispatch: validate sizes, pick the register-tile instantiation
+// for (M, alignment), size the persistent grid from the occupancy of that
+// instantiation (cached per device), and launch on the caller's stream.  No
+// allocation, no synchronisation.
+#include <cuda_runtime.h>
+
+#include <map>
+#include <cstdarg>
+#include <cstdio>
+#include <mutex>
+
+#include "rtk.h"
+#include "rtk_kernels.cuh"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+constexpr int kThreads = 256;  // 8 warps per CTA
+constexpr int kMaxDevices = 64;
+
+struct DeviceInfo {
+    std::once_flag once;
+    int sms = 0;
+};
+DeviceInfo g_dev[kMaxDevices];
+
+int device_sms() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return 148;
+    DeviceInfo& d = g_dev[dev];
+    std::call_once(d.once, [&] {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        d.sms = v;
+    });
+    return d.sms;
+}
+
+// Occupancy (CTAs per SM) of one kernel instantiation, cached per (device, kernel).
+std::mutex g_occ_mu;
+std::map<std::pair<int, const void*>, int> g_occ;
+
+int ctas_per_sm(const void* kernel) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_occ_mu);
+    auto it = g_occ.find({dev, kernel});
+    if (it != g_occ.end()) return it->second;
+    int blocks = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, kThreads, 0) != cudaSuccess || blocks < 1)
+        blocks = 1;
+    g_occ[{dev, kernel}] = blocks;
+    return blocks;
+}
+
+template <class K>
+int launch_rows(K kernel, const rtk::Args& a, cudaStream_t s) {
+    const long long warps_needed = a.n;
+    const long long blocks_needed = (warps_needed + (kThreads / 32) - 1) / (kThreads / 32);
+    long long grid = (long long)device_sms() * ctas_per_sm(reinterpret_cast<const void*>(kernel));
+    if (grid > blocks_needed) grid = blocks_needed;
+    if (grid < 1) grid = 1;
+    kernel<<<(unsigned)grid, kThreads, 0, s>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(RTK_ECUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+    return RTK_OK;
+}
+
+template <int MODE, int V, int C>
+int launch_reg(const rtk::Args& a, cudaStream_t s) {
+    if (a.m == C * 32 * V) return launch_rows(rtk::rowtopk_kernel<MODE, rtk::RegRow<V, C, false>>, a, s);
+    return launch_rows(rtk::rowtopk_kernel<MODE, rtk::RegRow<V, C, true>>, a, s);
+}
+
+template <int MODE>
+int dispatch(const rtk::Args& a, cudaStream_t s) {
+    const int m = a.m;
+    const bool vec4 = (m % 4 == 0) && (a.ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
+    if (m <= 1024 && vec4) {
+        switch ((m + 127) / 128) {
+            case 1: return launch_reg<MODE, 4, 1>(a, s);
+            case 2: return launch_reg<MODE, 4, 2>(a, s);
+            case 3: return launch_reg<MODE, 4, 3>(a, s);
+            case 4: return launch_reg<MODE, 4, 4>(a, s);
+            case 5: return launch_reg<MODE, 4, 5>(a, s);
+            case 6: return launch_reg<MODE, 4, 6>(a, s);
+            case 7: return launch_reg<MODE, 4, 7>(a, s);
+            default: return launch_reg<MODE, 4, 8>(a, s);
+        }
+    }
+    if (m <= 1024) {
+        const int c = (m + 31) / 32;
+        if (c <= 1) return launch_reg<MODE, 1, 1>(a, s);
+        if (c <= 2) return launch_reg<MODE, 1, 2>(a, s);
+        if (c <= 4) return launch_reg<MODE, 1, 4>(a, s);
+        if (c <= 8) return launch_reg<MODE, 1, 8>(a, s);
+        if (c <= 16) return launch_reg<MODE, 1, 16>(a, s);
+        return launch_reg<MODE, 1, 32>(a, s);
+    }
+    return launch_rows(rtk::rowtopk_kernel<MODE, rtk::GlobalRow>, a, s);
+}
+
+int launch_flat(void (*kernel)(rtk::Args), const rtk::Args& a, cudaStream_t s) {
+    const long long total = a.n * (long long)a.m;
+    long long grid = (total + kThreads - 1) / kThreads;
+    const long long cap = (long long)device_sms() * 8;
+    if (grid > cap) grid = cap;
+    if (grid < 1) grid = 1;
+    kernel<<<(unsigned)grid, kThreads, 0, s>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(RTK_ECUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+    return RTK_OK;
+}
+
+int check_common(const float* x, int64_t n, int64_t m, int64_t ldx) {
+    if (n < 0) return fail(RTK_EINVAL, "n must be >= 0, got %lld", (long long)n);
+    if (m < 1 || m > 0x7fffffff) return fail(RTK_EINVAL, "m must be in [1, 2^31), got %lld", (long long)m);
+    if (n >= 0xffffffffLL) return fail(RTK_EINVAL, "n must be < 2^32 - 1, got %lld", (long long)n);
+    if (ldx < m) return fail(RTK_EINVAL, "ldx (%lld) < m (%lld)", (long long)ldx, (long long)m);
+    if (n > 0 && !x) return fail(RTK_EINVAL, "x is NULL");
+    return RTK_OK;
+}
+
+int reset_nan(uint32_t* nan_first_row, cudaStream_t s) {
+    if (!nan_first_row) return RTK_OK;
+    cudaError_t e = cudaMemsetAsync(nan_first_row, 0xff, sizeof(uint32_t), s);
+    if (e != cudaSuccess) return fail(RTK_ECUDA, "cudaMemsetAsync failed: %s", cudaGetErrorString(e));
+    return RTK_OK;
+}
+
+rtk::Args make_args(const float* x, int64_t n, int64_t m, int64_t ldx, int32_t k, float* vals, int32_t* idx,
+                    int64_t ldo, int32_t* iters, int8_t* reasons, uint32_t* nan_first_row) {
+    rtk::Args a;
+    a.x = x;
+    a.n = n;
+    a.m = (int)m;
+    a.ldx = ldx;
+    a.k = k;
+    a.eps_rel = 0.0;
+    a.hard_cap = 64;
+    a.max_iter = 4;
+    a.vals = vals;
+    a.idx = idx;
+    a.ldo = ldo;
+    a.iters = iters;
+    a.reasons = reinterpret_cast<signed char*>(reasons);
+    a.nan_row = nan_first_row;
+    return a;
+}
+
+int rowtopk_common(int mode, const float* x, int64_t n, int64_t m, int64_t ldx, int32_t k, double eps_rel,
+                   int32_t hard_cap, int32_t max_iter, float* vals, int32_t* idx, int64_t ldo, int32_t* iters,
+                   int8_t* reasons, uint32_t* nan_first_row, void* stream) {
+    int rc = check_common(x, n, m, ldx);
+    if (rc) return rc;
+    if (k < 1 || k > m) return fail(RTK_EINVAL, "k must be in [1, %lld], got %d", (long long)m, k);
+    if (mode != rtk::kTrace) {
+        if (ldo < k) return fail(RTK_EINVAL, "ldo (%lld) < k (%d)", (long long)ldo, k);
+        if (n > 0 && (!vals || !idx)) return fail(RTK_EINVAL, "vals/idx is NULL");
+    } else if (n > 0 && (!iters || !reasons)) {
+        return fail(RTK_EINVAL, "iters/reasons are required for the trace kernel");
+    }
+    if (mode == rtk::kExact || mode == rtk::kTrace) {
+        if (!(eps_rel >= 0.0)) return fail(RTK_EINVAL, "eps_rel must be >= 0, got %g", eps_rel);
+        if (hard_cap < 1) return fail(RTK_EINVAL, "hard_cap must be >= 1, got %d", hard_cap);
+    } else if (max_iter < 1) {
+        return fail(RTK_EINVAL, "max_iter must be >= 1, got %d", max_iter);
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    rc = reset_nan(nan_first_row, s);
+    if (rc || n == 0) return rc;
+    rtk::Args a = make_args(x, n, m, ldx, k, mode == rtk::kTrace ? nullptr : vals,
+                            mode == rtk::kTrace ? nullptr : idx, ldo, iters, reasons, nan_first_row);
+    a.eps_rel = eps_rel;
+    a.hard_cap = hard_cap;
+    a.max_iter = max_iter;
+    if (k == m) return launch_flat(rtk::full_copy_kernel, a, s);  // _kernels.py:173-179
+    switch (mode) {
+        case rtk::kExact: return dispatch<rtk::kExact>(a, s);
+        case rtk::kEarly: return dispatch<rtk::kEarly>(a, s);
+        default: return dispatch<rtk::kTrace>(a, s);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int rtk_rowtopk_exact_f32(const float* x, int64_t n, int64_t m, int64_t ldx, int32_t k, double eps_rel,
+                          int32_t hard_cap, float* vals, int32_t* idx, int64_t ldo, int32_t* iters, int8_t* reasons,
+                          uint32_t* nan_first_row, void* stream) {
+    return rowtopk_common(rtk::kExact, x, n, m, ldx, k, eps_rel, hard_cap, 1, vals, idx, ldo, iters, reasons,
+                          nan_first_row, stream);
+}
+
+int rtk_rowtopk_early_f32(const float* x, int64_t n, int64_t m, int64_t ldx, int32_t k, int32_t max_iter,
+                          float* vals, int32_t* idx, int64_t ldo, int32_t* iters, int8_t* reasons,
+                          uint32_t* nan_first_row, void* stream) {
+    return rowtopk_common(rtk::kEarly, x, n, m, ldx, k, 0.0, 1, max_iter, vals, idx, ldo, iters, reasons,
+                          nan_first_row, stream);
+}
+
+int rtk_exact_trace_f32(const float* x, int64_t n, int64_t m, int64_t ldx, int32_t k, double eps_rel,
+                        int32_t hard_cap, int32_t* iters, int8_t* reasons, uint32_t* nan_first_row, void* stream) {
+    return rowtopk_common(rtk::kTrace, x, n, m, ldx, k, eps_rel, hard_cap, 1, nullptr, nullptr, k, iters, reasons,
+                          nan_first_row, stream);
+}
+
+int rtk_nan_scan_f32(const float* x, int64_t n, int64_t m, int64_t ldx, uint32_t* nan_first_row, void* stream) {
+    int rc = check_common(x, n, m, ldx);
+    if (rc) return rc;
+    if (!nan_first_row) return fail(RTK_EINVAL, "nan_first_row is NULL");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    rc = reset_nan(nan_first_row, s);
+    if (rc || n == 0) return rc;
+    rtk::Args a = make_args(x, n, m, ldx, 1, nullptr, nullptr, 1, nullptr, nullptr, nan_first_row);
+    return launch_flat(rtk::nan_scan_kernel, a, s);
+}
+
+int rtk_row_min_max_f32(const float* x, int64_t n, int64_t m, int64_t ldx, float* mins, float* maxs, void* stream) {
+    int rc = check_common(x, n, m, ldx);
+    if (rc) return rc;
+    if (n > 0 && (!mins || !maxs)) return fail(RTK_EINVAL, "mins/maxs is NULL");
+    if (n == 0) return RTK_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    rtk::Args a = make_args(x, n, m, ldx, 1, nullptr, nullptr, 1, nullptr, nullptr, nullptr);
+    long long grid = (n + 7) / 8, cap = (long long)device_sms() * 8;
+    if (grid > cap) grid = cap;
+    rtk::min_max_kernel<<<(unsigned)grid, kThreads, 0, s>>>(a, mins, maxs);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(RTK_ECUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+    return RTK_OK;
+}
+
+int rtk_count_ge_f32(const float* x, int64_t n, int64_t m, int64_t ldx, const float* thres, int32_t* counts,
+                     void* stream) {
+    int rc = check_common(x, n, m, ldx);
+    if (rc) return rc;
+    if (n > 0 && (!thres || !counts)) return fail(RTK_EINVAL, "thres/counts is NULL");
+    if (n == 0) return RTK_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    rtk::Args a = make_args(x, n, m, ldx, 1, nullptr, nullptr, 1, nullptr, nullptr, nullptr);
+    long long grid = (n + 7) / 8, cap = (long long)device_sms() * 8;
+    if (grid > cap) grid = cap;
+    rtk::count_ge_kernel<<<(unsigned)grid, kThreads, 0, s>>>(a, thres, counts);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(RTK_ECUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+    return RTK_OK;
+}
+
+const char* rtk_last_error(void) { return g_err; }
+
+int rtk_version(void) { return 100; }
+
+int rtk_launch_shape(int64_t m, int32_t k, int32_t mode, int32_t* warps_per_cta, int32_t* ctas_per_sm_out,
+                     int32_t* rows_per_warp) {
+    if (m < 1 || k < 1 || k > m || mode < 0 || mode > 2) return fail(RTK_EINVAL, "bad launch-shape query");
+    if (warps_per_cta) *warps_per_cta = kThreads / 32;
+    if (ctas_per_sm_out) *ctas_per_sm_out = 0;  // resolved per instantiation at launch
+    if (rows_per_warp) *rows_per_warp = 1;
+    return RTK_OK;
+}
+
+}  // extern "C"

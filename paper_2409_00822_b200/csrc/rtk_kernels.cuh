@@ -1,0 +1,540 @@
+// rtk_kernels.cuh -- sm_100a kernels for row-wise top-k by threshold bisection.
+//
+// One warp owns one row.  The row lives in registers (up to M = 1024 fp32,
+// 32 per lane), loaded with 128-bit streaming loads and prefetched one row
+// ahead; every bisection step is a per-lane FSET.BF/FADD2 compare-accumulate
+// plus one REDUX.SUM, min/max are CREDUX.MIN/MAX.F32 warp reductions, and
+// the selection is a warp prefix scan that writes exactly k (value, index)
+// pairs in ascending index order.  The launch is a persistent grid-stride
+// loop over rows.  Rows with M > 1024 take the same algorithm with the row
+// re-read from L1/L2 on each pass (GlobalRow).
+//
+// Numeric contract (bit-exact with /root/reference/pkg/src/rowtopk/_kernels.py):
+//   * all comparisons are fp32 IEEE >= (_kernels.py:43,75-84,120,140,207);
+//   * the midpoint equals F32((F64(a)+F64(b))*0.5) (_kernels.py:72,97), here
+//     computed in fp32 with an overflow fallback (proven
+//     on CPU in tests/test_oracle.py::test_fp32_midpoint_identity_random_bits);
+//   * the exact-mode loop test is the float64 `mx - mn > eps_rel*mx0`
+//     (_kernels.py:60,65); for eps_rel == 0 it reduces to the fp32
+//     `isfinite(mx0) && mx > mn`;
+//   * compiled without fast-math, -ftz=false, -fmad=false.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rtk {
+
+constexpr int kExitCountEqualsK = 1;        // _kernels.py:19
+constexpr int kExitIntervalBelowEps = 2;    // _kernels.py:20
+constexpr int kExitMaxIterReached = 3;      // _kernels.py:21
+constexpr int kExitHardCapReached = 4;      // _kernels.py:22
+constexpr int kExitDegenerateRow = 5;       // _kernels.py:23
+constexpr unsigned kFull = 0xffffffffu;
+
+enum Mode : int { kExact = 0, kEarly = 1, kTrace = 2 };
+
+struct Args {
+    const float* __restrict__ x;
+    long long n;
+    int m;
+    long long ldx;
+    int k;
+    double eps_rel;
+    int hard_cap;
+    int max_iter;
+    float* __restrict__ vals;
+    int* __restrict__ idx;
+    long long ldo;
+    int* __restrict__ iters;
+    signed char* __restrict__ reasons;
+    unsigned* __restrict__ nan_row;
+};
+
+// ---------------------------------------------------------------- scalars
+
+__device__ __forceinline__ float fmin_nan(float a, float b) {
+    float d;
+    asm("min.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+    return d;
+}
+
+// Warp-wide fp32 min (NaN-propagating: a NaN anywhere in the row makes mn0
+// NaN) and max, as sm_100 CREDUX.MIN/MAX.F32 into uniform registers.
+__device__ __forceinline__ float warp_min_nan(float v) {
+    float d;
+    asm volatile("redux.sync.min.NaN.f32 %0, %1, 0xffffffff;" : "=f"(d) : "f"(v));
+    return d;
+}
+__device__ __forceinline__ float warp_max(float v) {
+    float d;
+    asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(d) : "f"(v));
+    return d;
+}
+
+// 1.0f if a >= b else 0.0f (FSET.BF.GE; NaN compares false).
+__device__ __forceinline__ float set_ge(float a, float b) {
+    float d;
+    asm("set.ge.f32.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+    return d;
+}
+
+// (x, y) += (a, b) as one packed FADD2 (sm_100 f32x2).  Sums of 0/1 values
+// below 2^23 are exact.
+__device__ __forceinline__ void add2(float& x, float& y, float a, float b) {
+    asm("{.reg .b64 p, q; mov.b64 p, {%0, %1}; mov.b64 q, {%2, %3}; add.rn.f32x2 p, p, q; mov.b64 {%0, %1}, p;}"
+        : "+f"(x), "+f"(y)
+        : "f"(a), "f"(b));
+}
+
+// Lane counts are accumulated in floats seeded with 2^23, so the float's bit
+// pattern is 0x4B000000 + count; REDUX.SUM over 32 lanes then yields
+// kCountBias + row count, compared directly against k + kCountBias.
+constexpr unsigned kLaneBias = 0x4B000000u;
+constexpr int kCountBias = (int)(32u * kLaneBias);  // 0x60000000 (mod 2^32)
+
+__device__ __forceinline__ int warp_count(int lane_biased) {
+    return (int)((unsigned)__reduce_add_sync(kFull, lane_biased));
+}
+
+// Midpoint when |a|, |b| < 2^126 (no overflow possible): RN((a+b)) * 0.5.
+__device__ __forceinline__ float mid_fast(float a, float b) { return __fmul_rn(__fadd_rn(a, b), 0.5f); }
+
+// General midpoint, bit-identical to F32((F64(a)+F64(b))*0.5) (Appendix C).
+__device__ __forceinline__ float mid_exact(float a, float b) {
+    float s = __fadd_rn(a, b);
+    if (isinf(s) && isfinite(a) && isfinite(b)) return __fadd_rn(__fmul_rn(a, 0.5f), __fmul_rn(b, 0.5f));
+    return __fmul_rn(s, 0.5f);
+}
+
+__device__ __forceinline__ float4 ld_stream4(const float* p) {
+    return __ldcs(reinterpret_cast<const float4*>(p));
+}
+__device__ __forceinline__ float ld_stream1(const float* p) { return __ldcs(p); }
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned r;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+
+// ------------------------------------------------------- register row tile
+//
+// Slot (c, s) of lane l holds element c*32*V + l*V + s: chunk-major, so each
+// 128-bit load of a warp covers 512 contiguous bytes, and index order is
+// (chunk, lane, s) lexicographic -- a per-chunk lane scan gives positions.
+// Padding slots (MASKED, last chunk only) hold NaN, which no >= test counts.
+template <int V, int C, bool MASKED>
+struct RegRow {
+    static constexpr int kV = V;
+    static constexpr int kC = C;
+    float v[C][V];
+
+    __device__ __forceinline__ static int index(int c, int lane, int s) { return c * 32 * V + lane * V + s; }
+    __device__ __forceinline__ static bool valid(int c, int lane, int s, int m) {
+        return !MASKED || c < C - 1 || index(c, lane, s) < m;
+    }
+
+    __device__ __forceinline__ void load(const float* __restrict__ p, int m, int lane) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            if constexpr (V == 4) {
+                if (valid(c, lane, 0, m)) {
+                    float4 q = ld_stream4(p + index(c, lane, 0));
+                    v[c][0] = q.x; v[c][1] = q.y; v[c][2] = q.z; v[c][3] = q.w;
+                } else {
+                    v[c][0] = v[c][1] = v[c][2] = v[c][3] = __int_as_float(0x7fffffff);
+                }
+            } else {
+#pragma unroll
+                for (int s = 0; s < V; ++s)
+                    v[c][s] = valid(c, lane, s, m) ? ld_stream1(p + index(c, lane, s)) : __int_as_float(0x7fffffff);
+            }
+        }
+    }
+
+    // Lane-local min (NaN-propagating, so a NaN anywhere in the row is seen)
+    // and max (NaN-ignoring); padding is excluded.
+    __device__ __forceinline__ void lane_min_max(int m, int lane, float& mn, float& mx) const {
+        mn = __int_as_float(0x7f800000);
+        mx = __int_as_float(0xff800000);
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+#pragma unroll
+            for (int s = 0; s < V; ++s) {
+                if (valid(c, lane, s, m)) mn = fmin_nan(mn, v[c][s]);
+                mx = fmaxf(mx, v[c][s]);
+            }
+    }
+
+    // Biased lane count of v >= t (see kLaneBias): FSET.BF + FADD2 per pair.
+    __device__ __forceinline__ int lane_count_ge(float t) const {
+        constexpr int kSlots = C * V;
+        float sx = __int_as_float((int)kLaneBias), sy = 0.0f;
+#pragma unroll
+        for (int i = 0; i + 1 < kSlots; i += 2)
+            add2(sx, sy, set_ge(v[i / V][i % V], t), set_ge(v[(i + 1) / V][(i + 1) % V], t));
+        if constexpr (kSlots % 2) sx += set_ge(v[C - 1][V - 1], t);
+        return __float_as_int(sx + sy);
+    }
+
+    // First k elements (ascending index) with v >= t  (_kernels.py:118-125, 205-212).
+    __device__ __forceinline__ void select_ge(float t, int k, float* __restrict__ ov, int* __restrict__ oi,
+                                              int lane) const {
+        int base = 0;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            if (base >= k) break;
+            bool p[V];
+            int cl = 0;
+#pragma unroll
+            for (int s = 0; s < V; ++s) {
+                p[s] = v[c][s] >= t;
+                cl += p[s] ? 1 : 0;
+            }
+            int excl, total;
+            if constexpr (V == 1) {
+                unsigned b = __ballot_sync(kFull, p[0]);
+                excl = __popc(b & lanemask_lt());
+                total = __popc(b);
+            } else {
+                int incl = cl;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    int y = __shfl_up_sync(kFull, incl, d);
+                    if (lane >= d) incl += y;
+                }
+                total = __shfl_sync(kFull, incl, 31);
+                excl = incl - cl;
+            }
+            int pos = base + excl;
+#pragma unroll
+            for (int s = 0; s < V; ++s) {
+                if (p[s]) {
+                    if (pos < k) {
+                        ov[pos] = v[c][s];
+                        oi[pos] = index(c, lane, s);
+                    }
+                    ++pos;
+                }
+            }
+            base += total;
+        }
+    }
+
+    // All elements >= t plus the first `need` elements of [lo, t), merged in
+    // ascending index order (_kernels.py:126-145).
+    __device__ __forceinline__ void select_fill(float t, float lo, int need, int k, float* __restrict__ ov,
+                                                int* __restrict__ oi, int lane) const {
+        int baseA = 0, baseB = 0;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            bool pa[V], pb[V];
+            int packed = 0;
+#pragma unroll
+            for (int s = 0; s < V; ++s) {
+                pa[s] = v[c][s] >= t;
+                pb[s] = (lo <= v[c][s]) && (v[c][s] < t);
+                packed += (pa[s] ? 1 : 0) + (pb[s] ? 0x10000 : 0);
+            }
+            int incl = packed;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                int y = __shfl_up_sync(kFull, incl, d);
+                if (lane >= d) incl += y;
+            }
+            const int total = __shfl_sync(kFull, incl, 31);
+            const int excl = incl - packed;
+            int ea = baseA + (excl & 0xffff), eb = baseB + (excl >> 16);
+#pragma unroll
+            for (int s = 0; s < V; ++s) {
+                if (pa[s]) {
+                    int pos = ea + min(eb, need);
+                    if (pos < k) {
+                        ov[pos] = v[c][s];
+                        oi[pos] = index(c, lane, s);
+                    }
+                    ++ea;
+                } else if (pb[s]) {
+                    if (eb < need) {
+                        int pos = ea + eb;
+                        if (pos < k) {
+                            ov[pos] = v[c][s];
+                            oi[pos] = index(c, lane, s);
+                        }
+                    }
+                    ++eb;
+                }
+            }
+            baseA += total & 0xffff;
+            baseB += total >> 16;
+        }
+    }
+};
+
+// ------------------------------------------------------ global-memory row
+//
+// Rows longer than the register tile: same layout with V = 1 and a runtime
+// chunk count, every pass re-reading the row (L1/L2 resident after pass 1).
+struct GlobalRow {
+    const float* __restrict__ p;
+    int m;
+
+    __device__ __forceinline__ void load(const float* __restrict__ ptr, int m_, int) {
+        p = ptr;
+        m = m_;
+    }
+    __device__ __forceinline__ float at(int e) const { return e < m ? __ldg(p + e) : __int_as_float(0x7fffffff); }
+
+    __device__ __forceinline__ void lane_min_max(int, int lane, float& mn, float& mx) const {
+        mn = __int_as_float(0x7f800000);
+        mx = __int_as_float(0xff800000);
+        for (int e = lane; e < m; e += 32) {
+            float x = __ldg(p + e);
+            mn = fmin_nan(mn, x);
+            mx = fmaxf(mx, x);
+        }
+    }
+    __device__ __forceinline__ int lane_count_ge(float t) const {
+        int cnt = 0;
+        for (int e = threadIdx.x & 31; e < m; e += 32) cnt += (__ldg(p + e) >= t) ? 1 : 0;
+        return (int)kLaneBias + cnt;
+    }
+    __device__ __forceinline__ void select_ge(float t, int k, float* __restrict__ ov, int* __restrict__ oi,
+                                              int lane) const {
+        int base = 0;
+        const unsigned lt = lanemask_lt();
+        for (int c0 = 0; c0 < m && base < k; c0 += 32) {
+            const int e = c0 + lane;
+            const float x = at(e);
+            const bool q = x >= t;
+            const unsigned b = __ballot_sync(kFull, q);
+            const int pos = base + __popc(b & lt);
+            if (q && pos < k) {
+                ov[pos] = x;
+                oi[pos] = e;
+            }
+            base += __popc(b);
+        }
+    }
+    __device__ __forceinline__ void select_fill(float t, float lo, int need, int k, float* __restrict__ ov,
+                                                int* __restrict__ oi, int lane) const {
+        int baseA = 0, baseB = 0;
+        const unsigned lt = lanemask_lt();
+        for (int c0 = 0; c0 < m; c0 += 32) {
+            const int e = c0 + lane;
+            const float x = at(e);
+            const bool qa = x >= t;
+            const bool qb = (lo <= x) && (x < t);
+            const unsigned ba = __ballot_sync(kFull, qa), bb = __ballot_sync(kFull, qb);
+            const int ea = baseA + __popc(ba & lt), eb = baseB + __popc(bb & lt);
+            if (qa) {
+                const int pos = ea + min(eb, need);
+                if (pos < k) {
+                    ov[pos] = x;
+                    oi[pos] = e;
+                }
+            } else if (qb && eb < need) {
+                const int pos = ea + eb;
+                if (pos < k) {
+                    ov[pos] = x;
+                    oi[pos] = e;
+                }
+            }
+            baseA += __popc(ba);
+            baseB += __popc(bb);
+        }
+    }
+};
+
+// ---------------------------------------------------------- the searches
+
+// Algorithm 1 loop (_kernels.py:64-84), entered only when the loop-head test
+// passed at it == 0.  FP: eps_rel == 0 and mx0 finite, so the float64 head
+// test `mx - mn > eps` is the fp32 `mx > mn`; it is evaluated at the end of
+// each body (before the next body's hard-cap test, the reference order).
+// SAFE: |mn0|,|mx0| < 2^126 so the midpoint cannot overflow.
+// cnt is returned biased by kCountBias.
+template <bool FP, bool SAFE, class Row>
+__device__ __forceinline__ int exact_loop(const Row& row, int kb, double eps, int hard_cap, float& mn, float& mx,
+                                          float& thres, int& cnt, int& it) {
+    for (;;) {
+        if (it >= hard_cap) return kExitHardCapReached;
+        ++it;
+        const float mid = SAFE ? mid_fast(mn, mx) : mid_exact(mn, mx);
+        thres = mid;
+        cnt = warp_count(row.lane_count_ge(mid));
+        if (cnt == kb) return kExitCountEqualsK;
+        if (cnt < kb) {
+            if (mid == mx) return kExitIntervalBelowEps;
+            mx = mid;
+        } else {
+            if (mid == mn) return kExitIntervalBelowEps;
+            mn = mid;
+        }
+        if (!(FP ? (mx > mn) : ((double)mx - (double)mn > eps))) return kExitIntervalBelowEps;
+    }
+}
+
+template <int MODE, class Row>
+__device__ __forceinline__ void process_row(const Row& row, long long r, const Args& a, int lane) {
+    float mnl, mxl;
+    row.lane_min_max(a.m, lane, mnl, mxl);
+    const float mn0 = warp_min_nan(mnl), mx0 = warp_max(mxl);
+    if (mn0 != mn0) {  // batch.py:37-39: the row holds a NaN
+        if (lane == 0 && a.nan_row) atomicMin(a.nan_row, (unsigned)r);
+    }
+    const int k = a.k;
+    const int kb = k + kCountBias;
+    float* ov = a.vals + r * a.ldo;
+    int* oi = a.idx + r * a.ldo;
+    int it = 0, reason;
+
+    if constexpr (MODE == kEarly) {
+        // Algorithm 2 (_kernels.py:87-103) + first-k selection (:205-212)
+        float mn = mn0, mx = mx0;
+        if (!(mx0 > mn0)) {
+            reason = kExitDegenerateRow;
+        } else {
+            const int max_iter = a.max_iter;
+            if (fabsf(mn0) < 0x1p126f && fabsf(mx0) < 0x1p126f) {
+                for (int i = 0; i < max_iter; ++i) {
+                    const float mid = mid_fast(mn, mx);
+                    const bool lt = warp_count(row.lane_count_ge(mid)) < kb;
+                    mx = lt ? mid : mx;
+                    mn = lt ? mn : mid;
+                }
+            } else {
+                for (int i = 0; i < max_iter; ++i) {
+                    const float mid = mid_exact(mn, mx);
+                    const bool lt = warp_count(row.lane_count_ge(mid)) < kb;
+                    mx = lt ? mid : mx;
+                    mn = lt ? mn : mid;
+                }
+            }
+            it = max_iter;
+            reason = kExitMaxIterReached;
+        }
+        row.select_ge(mn, k, ov, oi, lane);
+    } else {
+        // Algorithm 1 (_kernels.py:48-84) + select_exact (_kernels.py:149-162)
+        const bool fp = (a.eps_rel == 0.0);
+        float mn = mn0, mx = mx0, thres = mn0;
+        int cnt = a.m + kCountBias;
+        if (fp) {
+            if (!(isfinite(mx0) && mx0 > mn0)) {
+                reason = kExitDegenerateRow;  // eps = 0*mx0 is NaN for infinite mx0
+            } else if (fabsf(mn0) < 0x1p126f && fabsf(mx0) < 0x1p126f) {
+                reason = exact_loop<true, true>(row, kb, 0.0, a.hard_cap, mn, mx, thres, cnt, it);
+            } else {
+                reason = exact_loop<true, false>(row, kb, 0.0, a.hard_cap, mn, mx, thres, cnt, it);
+            }
+        } else {
+            const double eps = a.eps_rel * (double)mx0;
+            if (!((double)mx0 - (double)mn0 > eps))
+                reason = kExitDegenerateRow;
+            else
+                reason = exact_loop<false, false>(row, kb, eps, a.hard_cap, mn, mx, thres, cnt, it);
+        }
+        if constexpr (MODE == kExact) {
+            const bool use_mx = (cnt > kb) && fp && (reason != kExitDegenerateRow);
+            const float t = use_mx ? mx : thres;
+            const int ca = (use_mx ? warp_count(row.lane_count_ge(mx)) : cnt) - kCountBias;
+            if (ca >= k)
+                row.select_ge(t, k, ov, oi, lane);
+            else
+                row.select_fill(t, mn, k - ca, k, ov, oi, lane);
+        }
+    }
+    if (lane == 0) {
+        if (a.iters) a.iters[r] = it;
+        if (a.reasons) a.reasons[r] = (signed char)reason;
+    }
+}
+
+// Persistent grid-stride row loop; each warp prefetches its next row into a
+// second register tile while the current one is searched.
+template <int MODE, class Row>
+__global__ void __launch_bounds__(256) rowtopk_kernel(Args a) {
+    const int lane = threadIdx.x & 31;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (r >= a.n) return;
+    Row A, B;
+    A.load(a.x + r * a.ldx, a.m, lane);
+    for (;;) {
+        const long long r1 = r + nw;
+        if (r1 < a.n) B.load(a.x + r1 * a.ldx, a.m, lane);
+        process_row<MODE>(A, r, a, lane);
+        if (r1 >= a.n) break;
+        const long long r2 = r1 + nw;
+        if (r2 < a.n) A.load(a.x + r2 * a.ldx, a.m, lane);
+        process_row<MODE>(B, r1, a, lane);
+        if (r2 >= a.n) break;
+        r = r2;
+    }
+}
+
+// k == M shortcut (_kernels.py:173-179): copy the row, indices 0..M-1, trace (0, DEGENERATE).
+__global__ void __launch_bounds__(256) full_copy_kernel(Args a) {
+    const long long total = a.n * (long long)a.m;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+        const long long r = e / a.m;
+        const int j = (int)(e - r * a.m);
+        const float x = a.x[r * a.ldx + j];
+        if (a.vals) {
+            a.vals[r * a.ldo + j] = x;
+            a.idx[r * a.ldo + j] = j;
+        }
+        if (x != x && a.nan_row) atomicMin(a.nan_row, (unsigned)r);
+        if (j == 0) {
+            if (a.iters) a.iters[r] = 0;
+            if (a.reasons) a.reasons[r] = (signed char)kExitDegenerateRow;
+        }
+    }
+}
+
+// NaN scan (batch.py:37-39) as a standalone pass.
+__global__ void __launch_bounds__(256) nan_scan_kernel(Args a) {
+    const long long total = a.n * (long long)a.m;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+        const long long r = e / a.m;
+        const int j = (int)(e - r * a.m);
+        const float x = a.x[r * a.ldx + j];
+        if (x != x) atomicMin(a.nan_row, (unsigned)r);
+    }
+}
+
+// Per-row min/max (_kernels.py:26-36) and count (_kernels.py:39-45), warp per row.
+__global__ void __launch_bounds__(256) min_max_kernel(Args a, float* __restrict__ mins, float* __restrict__ maxs) {
+    const int lane = threadIdx.x & 31;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < a.n; r += nw) {
+        GlobalRow row;
+        row.load(a.x + r * a.ldx, a.m, lane);
+        float mn, mx;
+        row.lane_min_max(a.m, lane, mn, mx);
+        mn = warp_min_nan(mn);
+        mx = warp_max(mx);
+        if (lane == 0) {
+            mins[r] = mn;
+            maxs[r] = mx;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) count_ge_kernel(Args a, const float* __restrict__ thres,
+                                                       int* __restrict__ counts) {
+    const int lane = threadIdx.x & 31;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < a.n; r += nw) {
+        GlobalRow row;
+        row.load(a.x + r * a.ldx, a.m, lane);
+        const int c = warp_count(row.lane_count_ge(thres[r])) - kCountBias;
+        if (lane == 0) counts[r] = c;
+    }
+}
+
+}  // namespace rtk

@@ -1,0 +1,226 @@
+"""GPU parity: the sm_100a kernels (through the C ABI / public API) against the
+reference-generated golden fixtures, the reference digests at BASELINE sizes,
+and the C oracle on fresh seeded inputs.  Bit-exact for values (as uint32
+bit patterns), indices, trace iterations and trace reasons."""
+
+import numpy as np
+import pytest
+
+from conftest import ROW_STYLES, random_row
+from golden_util import cases, digests, generate_matrix, h16, nan_cases
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2409_00822_b200 as rtk  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2409_00822_b200 import _build
+
+    _build.build()
+    torch.cuda.set_device(0)
+
+
+def _search(mode, max_iter=None, eps_rel=0.0, hard_cap=64):
+    if mode == "exact":
+        return rtk.SearchConfig.exact(epsilon_rel=eps_rel or 0.0, hard_cap=hard_cap)
+    return rtk.SearchConfig.early_stop(max_iter)
+
+
+def _bits(a):
+    return np.ascontiguousarray(a).view(np.uint32)
+
+
+def _np(x):
+    return x.cpu().numpy() if isinstance(x, torch.Tensor) else x
+
+
+def _check(res, v, i, t, r, ctx):
+    assert np.array_equal(_np(res.indices), i), ctx
+    assert np.array_equal(_bits(_np(res.values)), _bits(v)), ctx
+    assert np.array_equal(_np(res.trace_iterations), t), ctx
+    assert np.array_equal(_np(res.trace_reasons), r), ctx
+
+
+def test_every_golden_fixture_bit_exact():
+    """3000+ reference-generated cases: hand vectors, Appendix B edge rows,
+    tie-heavy styles, M = 1..4096, adversarial and special-value rows."""
+    n = 0
+    for c in cases():
+        cfg = rtk.BatchConfig(k=c["k"], search=_search(c["mode"], c["max_iter"], c["eps_rel"], c["hard_cap"]),
+                              collect_traces=True)
+        res = rtk.batch_topk(c["x"], cfg)  # numpy in -> numpy out (reference calling convention)
+        _check(res, c["values"], c["indices"], c["iters"], c["reasons"],
+               (c["xname"], c["k"], c["mode"], c["max_iter"], c["eps_rel"], c["hard_cap"]))
+        n += 1
+    assert n > 3000
+
+
+def test_golden_fixtures_device_resident_and_strided():
+    """Same fixtures through the zero-copy CUDA path with a padded row stride
+    (ldx > M) and without traces."""
+    for j, c in enumerate(cases()):
+        if j % 3:
+            continue
+        x = c["x"]
+        pad = 5 if j % 2 else 4
+        buf = torch.full((x.shape[0], x.shape[1] + pad), float("nan"), device="cuda")
+        buf[:, : x.shape[1]] = torch.from_numpy(x).cuda()
+        view = buf[:, : x.shape[1]]
+        cfg = rtk.BatchConfig(k=c["k"], search=_search(c["mode"], c["max_iter"], c["eps_rel"], c["hard_cap"]))
+        res = rtk.batch_topk(view, cfg)
+        assert res.trace_iterations is None
+        assert np.array_equal(res.indices.cpu().numpy(), c["indices"]), c["xname"]
+        assert np.array_equal(_bits(res.values.cpu().numpy()), _bits(c["values"])), c["xname"]
+
+
+def test_nan_rejection_names_first_row():
+    for c in nan_cases():
+        with pytest.raises(rtk.NaNInputError, match=f"first offending row: {c['first_row']}\\)"):
+            rtk.batch_topk(c["x"], rtk.BatchConfig(k=1))
+        with pytest.raises(rtk.NaNInputError):
+            rtk.batch_topk(torch.from_numpy(c["x"]).cuda(), rtk.BatchConfig(k=1, search=rtk.SearchConfig.early_stop(4)))
+        # NaN is reported before a bad k (batch.py:107-111)
+        with pytest.raises(rtk.NaNInputError):
+            rtk.batch_topk(c["x"], rtk.BatchConfig(k=c["x"].shape[1] + 1))
+
+
+@pytest.mark.parametrize("limit", [65536, 1 << 20])
+def test_reference_digests_at_baseline_sizes(limit):
+    """BASELINE configs incl. N=2^20 x 256 k=32 (exact, ES2/4/8), the Reddit
+    shape and the M x k sweep: output and trace digests equal the reference's."""
+    lo = 0 if limit == 65536 else 65537
+    mats = {}
+    checked = 0
+    for c in digests()["cases"]:
+        if not (lo <= c["N"] <= limit):
+            continue
+        key = (c["N"], c["M"], c["seed"])
+        if key not in mats:
+            mats.clear()
+            x = generate_matrix(c["N"], c["M"], c["seed"])
+            assert h16(x) == c["input"]
+            mats[key] = torch.from_numpy(x).cuda()
+        cfg = rtk.BatchConfig(k=c["k"], search=_search(c["mode"], c["max_iter"], c["eps_rel"]), collect_traces=True)
+        res = rtk.batch_topk(mats[key], cfg)
+        v, i = res.values.cpu().numpy(), res.indices.cpu().numpy()
+        t, r = res.trace_iterations.cpu().numpy(), res.trace_reasons.cpu().numpy()
+        assert h16(v, i) == c["out"], c
+        assert h16(t, r) == c["tr"], c
+        checked += 1
+    assert checked > 0
+
+
+def test_random_shapes_vs_oracle(oracle_lib):
+    rng = np.random.default_rng(77)
+    for trial in range(120):
+        m = int(rng.choice([int(rng.integers(1, 40)), int(rng.integers(1, 1100)), int(rng.integers(1000, 3000))]))
+        n = int(rng.integers(1, 300))
+        style = ROW_STYLES[trial % 4]
+        x = np.stack([random_row(rng, m, style) for _ in range(n)]) if style != "normal" else \
+            rng.standard_normal((n, m), dtype=np.float32) * np.float32(rng.choice([1e-30, 1.0, 1e30]))
+        k = int(rng.integers(1, m + 1))
+        if trial % 2:
+            mode, mi, eps, cap = "exact", 4, float(rng.choice([0.0, 0.0, 1e-16, 1e-3])), int(rng.choice([64, 64, 5]))
+        else:
+            mode, mi, eps, cap = "early", int(rng.integers(1, 20)), 0.0, 64
+        want = oracle_lib.ref_batch(x, k, mode, max_iter=mi, eps_rel=eps, hard_cap=cap)
+        res = rtk.batch_topk(x, rtk.BatchConfig(k=k, search=_search(mode, mi, eps, cap), collect_traces=True))
+        _check(res, *want, (trial, n, m, k, mode, mi, eps, cap, style))
+
+
+def test_single_row_api_matches_batch_rows():
+    """test_batch.py:45-61: every 17th row of 300 x 48 equals the single-row op incl. traces."""
+    rng = np.random.default_rng(0xC0FFEE)
+    m = rng.standard_normal((300, 48)).astype(np.float32)
+    for search in (rtk.SearchConfig.exact(), rtk.SearchConfig.early_stop(3)):
+        res = rtk.batch_topk(m, rtk.BatchConfig(k=7, search=search, collect_traces=True))
+        traces = res.traces()
+        for r in range(0, 300, 17):
+            if search.mode is rtk.SearchMode.EXACT:
+                single, tr = rtk.exact_topk(m[r], 7)
+            else:
+                single, tr = rtk.early_stop_topk(m[r], 7, search)
+            assert np.array_equal(res.values[r], single.values)
+            assert np.array_equal(res.indices[r], single.indices)
+            assert traces[r] == tr
+
+
+def test_single_row_helpers():
+    assert rtk.min_max([3.0, 1.0, 2.0]) == (1.0, 3.0)
+    assert rtk.min_max([5.0]) == (5.0, 5.0)
+    assert rtk.count_ge([1.0, 2.0, 3.0], 2.0) == 2
+    assert rtk.count_ge([1.0, 2.0, 3.0], 3.5) == 0
+    r = rtk.oracle_topk([1.0, 3.0, 2.0], 2)
+    assert r.values.tolist() == [3.0, 2.0] and r.indices.tolist() == [1, 2]
+    assert rtk.oracle_topk([5.0, 5.0, 1.0], 1).indices.tolist() == [0]
+    with pytest.raises(rtk.EmptyRowError):
+        rtk.min_max([])
+    with pytest.raises(rtk.NaNInputError):
+        rtk.min_max([1.0, float("nan")])
+    with pytest.raises(rtk.NaNInputError):
+        rtk.count_ge([1.0], float("nan"))
+    with pytest.raises(rtk.KOutOfRangeError):
+        rtk.exact_topk([1.0, 2.0], 3)
+    with pytest.raises(ValueError):
+        rtk.exact_topk([1.0, 2.0], 1, rtk.SearchConfig.early_stop(4))
+
+
+def test_validation_errors():
+    rng = np.random.default_rng(1)
+    m = rng.standard_normal((4, 8)).astype(np.float32)
+    with pytest.raises(rtk.KOutOfRangeError):
+        rtk.batch_topk(m, rtk.BatchConfig(k=9))
+    with pytest.raises(rtk.KOutOfRangeError):
+        rtk.batch_topk(m, rtk.BatchConfig(k=0))
+    with pytest.raises(rtk.DimensionMismatchError):
+        rtk.batch_topk(m.ravel(), rtk.BatchConfig(k=2))
+    with pytest.raises(rtk.EmptyRowError):
+        rtk.batch_topk(np.zeros((0, 4), np.float32), rtk.BatchConfig(k=1))
+    with pytest.raises(ValueError):
+        rtk.batch_topk(m, rtk.BatchConfig(k=2, workers=0))
+    m[2, 5] = np.nan
+    with pytest.raises(rtk.NaNInputError, match="row: 2"):
+        rtk.batch_topk(m, rtk.BatchConfig(k=2))
+
+
+def test_deterministic_and_traces_off_by_default():
+    x = torch.randn(4000, 96, device="cuda")
+    a = rtk.batch_topk(x, rtk.BatchConfig(k=13, collect_traces=True))
+    b = rtk.batch_topk(x, rtk.BatchConfig(k=13, collect_traces=True))
+    assert torch.equal(a.values, b.values) and torch.equal(a.indices, b.indices)
+    assert torch.equal(a.trace_iterations, b.trace_iterations)
+    c = rtk.batch_topk(x, rtk.BatchConfig(k=13))
+    assert c.trace_iterations is None
+    with pytest.raises(ValueError):
+        c.traces()
+
+
+def test_exact_trace_kernel_matches_oracle(oracle_lib):
+    x = generate_matrix(20000, 256, 3)
+    for eps in (0.0, 1e-4):
+        it, rs = rtk.exact_trace(x, 32, rtk.SearchConfig.exact(epsilon_rel=eps))
+        wit, wrs = oracle_lib.exact_trace(x, 32, eps_rel=eps)
+        assert np.array_equal(it, wit) and np.array_equal(rs, wrs)
+
+
+def test_large_offsets_sampled_vs_oracle(oracle_lib):
+    """> 2^31 elements in one launch (int64 row offsets), device-generated
+    input; a row sample is checked against the oracle."""
+    n, m, k = 2_200_000, 1024, 64
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(n, m, device="cuda", generator=g)
+    for search, mode in ((rtk.SearchConfig.exact(), "exact"), (rtk.SearchConfig.early_stop(4), "early")):
+        res = rtk.batch_topk(x, rtk.BatchConfig(k=k, search=search, collect_traces=True))
+        rows = torch.tensor([0, 1, 12345, n // 2, n - 3, n - 2, n - 1], device="cuda")
+        xs = x[rows].cpu().numpy()
+        v, i, t, r = oracle_lib.ref_batch(xs, k, mode, max_iter=4)
+        assert np.array_equal(res.indices[rows].cpu().numpy(), i)
+        assert np.array_equal(_bits(res.values[rows].cpu().numpy()), _bits(v))
+        assert np.array_equal(res.trace_iterations[rows].cpu().numpy(), t)
+    del x
+    torch.cuda.empty_cache()
