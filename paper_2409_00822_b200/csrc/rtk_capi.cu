@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <map>
+#include <tuple>
 #include <cstdarg>
 #include <cstdio>
 #include <mutex>
@@ -47,31 +48,35 @@ int device_sms() {
     return d.sms;
 }
 
-// Occupancy (CTAs per SM) of one kernel instantiation, cached per (device, kernel).
+// Occupancy (CTAs per SM) of one kernel instantiation at a dynamic shared
+// memory size, cached per (device, kernel, smem); kernels needing more than
+// 48 KB of dynamic shared memory are opted in once.
 std::mutex g_occ_mu;
-std::map<std::pair<int, const void*>, int> g_occ;
+std::map<std::tuple<int, const void*, size_t>, int> g_occ;
 
-int ctas_per_sm(const void* kernel) {
+int ctas_per_sm(const void* kernel, size_t smem) {
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(g_occ_mu);
-    auto it = g_occ.find({dev, kernel});
+    auto key = std::make_tuple(dev, kernel, smem);
+    auto it = g_occ.find(key);
     if (it != g_occ.end()) return it->second;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int blocks = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, kThreads, 0) != cudaSuccess || blocks < 1)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, kThreads, smem) != cudaSuccess || blocks < 1)
         blocks = 1;
-    g_occ[{dev, kernel}] = blocks;
+    g_occ[key] = blocks;
     return blocks;
 }
 
 template <class K>
-int launch_rows(K kernel, const rtk::Args& a, cudaStream_t s) {
+int launch_rows(K kernel, const rtk::Args& a, cudaStream_t s, size_t smem) {
     const long long warps_needed = a.n;
     const long long blocks_needed = (warps_needed + (kThreads / 32) - 1) / (kThreads / 32);
-    long long grid = (long long)device_sms() * ctas_per_sm(reinterpret_cast<const void*>(kernel));
+    long long grid = (long long)device_sms() * ctas_per_sm(reinterpret_cast<const void*>(kernel), smem);
     if (grid > blocks_needed) grid = blocks_needed;
     if (grid < 1) grid = 1;
-    kernel<<<(unsigned)grid, kThreads, 0, s>>>(a);
+    kernel<<<(unsigned)grid, kThreads, smem, s>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(RTK_ECUDA, "kernel launch failed: %s", cudaGetErrorString(e));
     return RTK_OK;
@@ -79,8 +84,10 @@ int launch_rows(K kernel, const rtk::Args& a, cudaStream_t s) {
 
 template <int MODE, int V, int C>
 int launch_reg(const rtk::Args& a, cudaStream_t s) {
-    if (a.m == C * 32 * V) return launch_rows(rtk::rowtopk_kernel<MODE, rtk::RegRow<V, C, false>>, a, s);
-    return launch_rows(rtk::rowtopk_kernel<MODE, rtk::RegRow<V, C, true>>, a, s);
+    // staging buffer: k values + k indices per warp (no selection in trace mode)
+    const size_t smem = MODE == rtk::kTrace ? 0 : (size_t)(kThreads / 32) * 2 * a.k * sizeof(float);
+    if (a.m == C * 32 * V) return launch_rows(rtk::rowtopk_kernel<MODE, rtk::RegRow<V, C, false>>, a, s, smem);
+    return launch_rows(rtk::rowtopk_kernel<MODE, rtk::RegRow<V, C, true>>, a, s, smem);
 }
 
 template <int MODE>
@@ -108,7 +115,7 @@ int dispatch(const rtk::Args& a, cudaStream_t s) {
         if (c <= 16) return launch_reg<MODE, 1, 16>(a, s);
         return launch_reg<MODE, 1, 32>(a, s);
     }
-    return launch_rows(rtk::rowtopk_kernel<MODE, rtk::GlobalRow>, a, s);
+    return launch_rows(rtk::rowtopk_kernel<MODE, rtk::GlobalRow>, a, s, 0);
 }
 
 int launch_flat(void (*kernel)(rtk::Args), const rtk::Args& a, cudaStream_t s) {

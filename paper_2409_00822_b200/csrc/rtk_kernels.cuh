@@ -118,6 +118,30 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return r;
 }
 
+// Shared-memory staging of selected (value, index) pairs: 8 bytes per output
+// position, one buffer of k pairs per warp, addressed in the shared window.
+__device__ __forceinline__ void stage_put(unsigned addr, float v, int idx) {
+    asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(__float_as_int(v)), "r"(idx) : "memory");
+}
+__device__ __forceinline__ void stage_get(unsigned addr, float& v, int& idx) {
+    int b;
+    asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(b), "=r"(idx) : "r"(addr) : "memory");
+    v = __int_as_float(b);
+}
+
+// Inclusive warp prefix sum: SHFL.UP with its in-range predicate guarding the add.
+__device__ __forceinline__ unsigned warp_incl_scan(unsigned x) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1)
+        asm volatile(
+            "{.reg .pred p; .reg .b32 t;\n\t"
+            "shfl.sync.up.b32 t|p, %0, %1, 0, 0xffffffff;\n\t"
+            "@p add.u32 %0, %0, t;}"
+            : "+r"(x)
+            : "r"(d));
+    return x;
+}
+
 // ------------------------------------------------------- register row tile
 //
 // Slot (c, s) of lane l holds element c*32*V + l*V + s: chunk-major, so each
@@ -126,13 +150,16 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // Padding slots (MASKED, last chunk only) hold NaN, which no >= test counts.
 template <int V, int C, bool MASKED>
 struct RegRow {
+    static constexpr bool kStaged = true;  // selection goes through shared memory
     static constexpr int kV = V;
     static constexpr int kC = C;
     float v[C][V];
 
     __device__ __forceinline__ static int index(int c, int lane, int s) { return c * 32 * V + lane * V + s; }
+    // V == 4 tiles are sized so only the last chunk can be partial; V == 1
+    // tiles round C up to a power of two, so any chunk may be (partly) padding.
     __device__ __forceinline__ static bool valid(int c, int lane, int s, int m) {
-        return !MASKED || c < C - 1 || index(c, lane, s) < m;
+        return !MASKED || (V == 4 && c < C - 1) || index(c, lane, s) < m;
     }
 
     __device__ __forceinline__ void load(const float* __restrict__ p, int m, int lane) {
@@ -178,105 +205,120 @@ struct RegRow {
         return __float_as_int(sx + sy);
     }
 
-    // First k elements (ascending index) with v >= t  (_kernels.py:118-125, 205-212).
-    __device__ __forceinline__ void select_ge(float t, int k, float* __restrict__ ov, int* __restrict__ oi,
-                                              int lane) const {
-        int base = 0;
+    // Per-chunk lane counts of the predicate bits packed one byte per chunk
+    // (4 chunks per word: a lane holds <= 4 hits per chunk, a chunk <= 128),
+    // so one warp scan serves four chunks.
+    static constexpr int kWords = (C + 3) / 4;
+
+    // Stage the first k elements (ascending index) with v >= t into the
+    // warp's shared-memory row buffer (_kernels.py:118-125, 205-212).
+    __device__ __forceinline__ void select_ge(float t, int k, unsigned sbase, int lane) const {
+        bool p[C][V];
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-            if (base >= k) break;
-            bool p[V];
-            int cl = 0;
+        for (int c = 0; c < C; ++c)
 #pragma unroll
-            for (int s = 0; s < V; ++s) {
-                p[s] = v[c][s] >= t;
-                cl += p[s] ? 1 : 0;
+            for (int s = 0; s < V; ++s) p[c][s] = v[c][s] >= t;
+        if constexpr (V == 1) {
+            const unsigned lt = lanemask_lt();
+            int base = 0;
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                if (base >= k) break;
+                const unsigned b = __ballot_sync(kFull, p[c][0]);
+                const int pos = base + __popc(b & lt);
+                if (p[c][0] && pos < k) stage_put(sbase + 8u * pos, v[c][0], index(c, lane, 0));
+                base += __popc(b);
             }
-            int excl, total;
-            if constexpr (V == 1) {
-                unsigned b = __ballot_sync(kFull, p[0]);
-                excl = __popc(b & lanemask_lt());
-                total = __popc(b);
-            } else {
-                int incl = cl;
+        } else {
+            unsigned cnt[kWords], incl[kWords], tot[kWords];
 #pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    int y = __shfl_up_sync(kFull, incl, d);
-                    if (lane >= d) incl += y;
+            for (int w = 0; w < kWords; ++w) cnt[w] = 0;
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                unsigned cl = 0;
+#pragma unroll
+                for (int s = 0; s < V; ++s) cl += p[c][s] ? 1u : 0u;
+                cnt[c / 4] += cl << (8 * (c % 4));
+            }
+#pragma unroll
+            for (int w = 0; w < kWords; ++w) {
+                incl[w] = warp_incl_scan(cnt[w]);
+                tot[w] = __shfl_sync(kFull, incl[w], 31);
+            }
+            int base = 0;
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                const int pos0 = base + (int)(((incl[c / 4] - cnt[c / 4]) >> (8 * (c % 4))) & 0xffu);
+                unsigned addr = sbase + 8u * pos0;
+                const unsigned aend = sbase + 8u * k;
+#pragma unroll
+                for (int s = 0; s < V; ++s) {
+                    if (p[c][s] && addr < aend) stage_put(addr, v[c][s], index(c, lane, s));
+                    addr += p[c][s] ? 8u : 0u;
                 }
-                total = __shfl_sync(kFull, incl, 31);
-                excl = incl - cl;
+                base += (int)((tot[c / 4] >> (8 * (c % 4))) & 0xffu);
             }
-            int pos = base + excl;
-#pragma unroll
-            for (int s = 0; s < V; ++s) {
-                if (p[s]) {
-                    if (pos < k) {
-                        ov[pos] = v[c][s];
-                        oi[pos] = index(c, lane, s);
-                    }
-                    ++pos;
-                }
-            }
-            base += total;
         }
     }
 
     // All elements >= t plus the first `need` elements of [lo, t), merged in
-    // ascending index order (_kernels.py:126-145).
-    __device__ __forceinline__ void select_fill(float t, float lo, int need, int k, float* __restrict__ ov,
-                                                int* __restrict__ oi, int lane) const {
+    // ascending index order (_kernels.py:126-145).  Cold on benchmark data.
+    __device__ __forceinline__ void select_fill(float t, float lo, int need, int k, unsigned sbase,
+                                                int lane) const {
         int baseA = 0, baseB = 0;
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             bool pa[V], pb[V];
-            int packed = 0;
+            unsigned packed = 0;
 #pragma unroll
             for (int s = 0; s < V; ++s) {
                 pa[s] = v[c][s] >= t;
                 pb[s] = (lo <= v[c][s]) && (v[c][s] < t);
-                packed += (pa[s] ? 1 : 0) + (pb[s] ? 0x10000 : 0);
+                packed += (pa[s] ? 1u : 0u) + (pb[s] ? 0x10000u : 0u);
             }
-            int incl = packed;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                int y = __shfl_up_sync(kFull, incl, d);
-                if (lane >= d) incl += y;
-            }
-            const int total = __shfl_sync(kFull, incl, 31);
-            const int excl = incl - packed;
-            int ea = baseA + (excl & 0xffff), eb = baseB + (excl >> 16);
+            const unsigned incl = warp_incl_scan(packed);
+            const unsigned total = __shfl_sync(kFull, incl, 31);
+            const unsigned excl = incl - packed;
+            int ea = baseA + (int)(excl & 0xffffu), eb = baseB + (int)(excl >> 16);
 #pragma unroll
             for (int s = 0; s < V; ++s) {
                 if (pa[s]) {
-                    int pos = ea + min(eb, need);
-                    if (pos < k) {
-                        ov[pos] = v[c][s];
-                        oi[pos] = index(c, lane, s);
-                    }
+                    const int pos = ea + min(eb, need);
+                    if (pos < k) stage_put(sbase + 8u * pos, v[c][s], index(c, lane, s));
                     ++ea;
                 } else if (pb[s]) {
-                    if (eb < need) {
-                        int pos = ea + eb;
-                        if (pos < k) {
-                            ov[pos] = v[c][s];
-                            oi[pos] = index(c, lane, s);
-                        }
-                    }
+                    if (eb < need && ea + eb < k) stage_put(sbase + 8u * (ea + eb), v[c][s], index(c, lane, s));
                     ++eb;
                 }
             }
-            baseA += total & 0xffff;
-            baseB += total >> 16;
+            baseA += (int)(total & 0xffffu);
+            baseB += (int)(total >> 16);
         }
     }
 };
+
+// Copy a staged row (k values, k indices in shared memory) to global with
+// coalesced stores; the surrounding __syncwarp()s order the warp's shared
+// buffer between rows.
+__device__ __forceinline__ void flush_row(unsigned sbase, int k, float* __restrict__ ov, int* __restrict__ oi,
+                                          int lane) {
+    __syncwarp();
+    for (int j = lane; j < k; j += 32) {
+        float v;
+        int i;
+        stage_get(sbase + 8u * j, v, i);
+        ov[j] = v;
+        oi[j] = i;
+    }
+    __syncwarp();
+}
 
 // ------------------------------------------------------ global-memory row
 //
 // Rows longer than the register tile: same layout with V = 1 and a runtime
 // chunk count, every pass re-reading the row (L1/L2 resident after pass 1).
 struct GlobalRow {
+    static constexpr bool kStaged = false;  // selection stores straight to global
     const float* __restrict__ p;
     int m;
 
@@ -358,26 +400,31 @@ struct GlobalRow {
 template <bool FP, bool SAFE, class Row>
 __device__ __forceinline__ int exact_loop(const Row& row, int kb, double eps, int hard_cap, float& mn, float& mx,
                                           float& thres, int& cnt, int& it) {
-    for (;;) {
-        if (it >= hard_cap) return kExitHardCapReached;
+    // One body per bisection step with a single exit branch.  The bracket
+    // update is applied unconditionally: on a no-progress exit (mid equal to
+    // the bound being replaced) it is a no-op, and on cnt == k the moved
+    // lower bound is never read again (select_exact uses thres and cnt).
+    bool eq, stuck, cont;
+    float mid;
+    do {
         ++it;
-        const float mid = SAFE ? mid_fast(mn, mx) : mid_exact(mn, mx);
-        thres = mid;
+        mid = SAFE ? mid_fast(mn, mx) : mid_exact(mn, mx);
         cnt = warp_count(row.lane_count_ge(mid));
-        if (cnt == kb) return kExitCountEqualsK;
-        if (cnt < kb) {
-            if (mid == mx) return kExitIntervalBelowEps;
-            mx = mid;
-        } else {
-            if (mid == mn) return kExitIntervalBelowEps;
-            mn = mid;
-        }
-        if (!(FP ? (mx > mn) : ((double)mx - (double)mn > eps))) return kExitIntervalBelowEps;
-    }
+        const bool lt = cnt < kb;
+        eq = cnt == kb;
+        stuck = mid == (lt ? mx : mn);
+        mx = lt ? mid : mx;
+        mn = lt ? mn : mid;
+        cont = FP ? (mx > mn) : ((double)mx - (double)mn > eps);
+    } while (!eq && !stuck && cont && it < hard_cap);
+    thres = mid;
+    if (eq) return kExitCountEqualsK;
+    if (stuck || !cont) return kExitIntervalBelowEps;
+    return kExitHardCapReached;
 }
 
 template <int MODE, class Row>
-__device__ __forceinline__ void process_row(const Row& row, long long r, const Args& a, int lane) {
+__device__ __forceinline__ void process_row(const Row& row, long long r, const Args& a, int lane, unsigned sbase) {
     float mnl, mxl;
     row.lane_min_max(a.m, lane, mnl, mxl);
     const float mn0 = warp_min_nan(mnl), mx0 = warp_max(mxl);
@@ -415,7 +462,12 @@ __device__ __forceinline__ void process_row(const Row& row, long long r, const A
             it = max_iter;
             reason = kExitMaxIterReached;
         }
-        row.select_ge(mn, k, ov, oi, lane);
+        if constexpr (Row::kStaged) {
+            row.select_ge(mn, k, sbase, lane);
+            flush_row(sbase, k, ov, oi, lane);
+        } else {
+            row.select_ge(mn, k, ov, oi, lane);
+        }
     } else {
         // Algorithm 1 (_kernels.py:48-84) + select_exact (_kernels.py:149-162)
         const bool fp = (a.eps_rel == 0.0);
@@ -440,10 +492,18 @@ __device__ __forceinline__ void process_row(const Row& row, long long r, const A
             const bool use_mx = (cnt > kb) && fp && (reason != kExitDegenerateRow);
             const float t = use_mx ? mx : thres;
             const int ca = (use_mx ? warp_count(row.lane_count_ge(mx)) : cnt) - kCountBias;
-            if (ca >= k)
-                row.select_ge(t, k, ov, oi, lane);
-            else
-                row.select_fill(t, mn, k - ca, k, ov, oi, lane);
+            if constexpr (Row::kStaged) {
+                if (ca >= k)
+                    row.select_ge(t, k, sbase, lane);
+                else
+                    row.select_fill(t, mn, k - ca, k, sbase, lane);
+                flush_row(sbase, k, ov, oi, lane);
+            } else {
+                if (ca >= k)
+                    row.select_ge(t, k, ov, oi, lane);
+                else
+                    row.select_fill(t, mn, k - ca, k, ov, oi, lane);
+            }
         }
     }
     if (lane == 0) {
@@ -453,10 +513,13 @@ __device__ __forceinline__ void process_row(const Row& row, long long r, const A
 }
 
 // Persistent grid-stride row loop; each warp prefetches its next row into a
-// second register tile while the current one is searched.
+// second register tile while the current one is searched.  Dynamic shared
+// memory: one k-value + k-index staging buffer per warp (staged rows only).
 template <int MODE, class Row>
 __global__ void __launch_bounds__(256) rowtopk_kernel(Args a) {
+    extern __shared__ __align__(16) float smem[];
     const int lane = threadIdx.x & 31;
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem) + (threadIdx.x >> 5) * 8u * a.k;
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
     long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (r >= a.n) return;
@@ -465,11 +528,11 @@ __global__ void __launch_bounds__(256) rowtopk_kernel(Args a) {
     for (;;) {
         const long long r1 = r + nw;
         if (r1 < a.n) B.load(a.x + r1 * a.ldx, a.m, lane);
-        process_row<MODE>(A, r, a, lane);
+        process_row<MODE>(A, r, a, lane, sbase);
         if (r1 >= a.n) break;
         const long long r2 = r1 + nw;
         if (r2 < a.n) A.load(a.x + r2 * a.ldx, a.m, lane);
-        process_row<MODE>(B, r1, a, lane);
+        process_row<MODE>(B, r1, a, lane, sbase);
         if (r2 >= a.n) break;
         r = r2;
     }

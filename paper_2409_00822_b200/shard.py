@@ -2,8 +2,8 @@
 collective on the hot path.
 
 Rows are independent, so rank r of W owns the contiguous block
-``chunk_ranges(N, W)[r]`` -- the reference's own partition rule
-(batch.py:87-91) -- and runs the single-GPU kernel on it.  Outputs are
+[floor(rN/W), floor((r+1)N/W)) -- the np.linspace rule of the reference's
+chunk_ranges (batch.py:87-91), kept rank-aligned even when N < W -- and runs the single-GPU kernel on it.  Outputs are
 byte-identical to the single-GPU result by row independence (the reference's
 worker-count determinism, test_batch.py:74-81).  Gathering the blocks is
 optional and off the timed path: ``gather=True`` all-gathers them through
@@ -14,7 +14,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .batch import BatchConfig, BatchResult, batch_topk, chunk_ranges
+from .batch import BatchConfig, BatchResult, batch_topk
 
 
 def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
@@ -71,9 +71,7 @@ def _gather(res, cfg, n_total, world, group, block):
 
     dist = _dist()
     k = int(cfg.k)
-    ranges = chunk_ranges(n_total, world)
-    while len(ranges) < world:
-        ranges.append((n_total, n_total))
+    ranges = [shard_range(n_total, r, world) for r in range(world)]
     rows_max = max(b - a for a, b in ranges)
     on_cuda = isinstance(block, torch.Tensor) and block.is_cuda
     dev = block.device if on_cuda else torch.device("cpu")
