@@ -58,6 +58,8 @@ def parse():
     p.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     p.add_argument("--mode", default="exact", choices=["exact", "early"])
     p.add_argument("--max-iter", type=int, default=4)
+    p.add_argument("--only-mode", action="store_true", help="time only --mode (for profiling)")
+    p.add_argument("--no-torch", action="store_true", help="skip the torch.topk comparison")
     p.add_argument("--strong", action="store_true", help="shard a fixed global N across ranks")
     p.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
     p.add_argument("--no-e2e", action="store_true")
@@ -301,6 +303,8 @@ def main():
     x = make_input(n, m, args.seed, rank, dev)
     dm = rtk.batch._DeviceMatrix(x)
     searches = {"exact": rtk.SearchConfig.exact(), "early": rtk.SearchConfig.early_stop(args.max_iter)}
+    if args.only_mode:
+        searches = {args.mode: searches[args.mode]}
     nan_word = dm._new_nan_word()
     outs = {md: dm.launch_topk(k, s, False, nan_word=nan_word) for md, s in searches.items()}
     torch.cuda.synchronize()
@@ -324,12 +328,12 @@ def main():
 
     # torch.topk on the same device-resident input (the paper's comparison point)
     tk = {}
-    for sorted_ in (True, False):
+    for sorted_ in (() if args.no_torch else (True, False)):
         ms = time_launches(lambda: torch.topk(x, k, dim=1, sorted=sorted_), max(5, args.steps // 10),
                            3, world, stream)
         tk["sorted" if sorted_ else "unsorted"] = {"ms_per_step": ms, "rows_per_s": world * n / (ms * 1e-3)}
     head = results[args.mode]
-    speedup_vs_torch = tk["sorted"]["ms_per_step"] / head["ms_per_step"]
+    speedup_vs_torch = tk["sorted"]["ms_per_step"] / head["ms_per_step"] if tk else None
 
     # e2e through the public API with pinned host buffers (H2D + kernel + D2H each step)
     e2e = None

@@ -90,20 +90,29 @@ int launch_reg(const rtk::Args& a, cudaStream_t s) {
     return launch_rows(rtk::rowtopk_kernel<MODE, rtk::RegRow<V, C, true>>, a, s, smem);
 }
 
+template <int MODE, int E>
+int launch_lane(const rtk::Args& a, cudaStream_t s) {
+    // staging buffer: 32*E (value, index) pairs per warp (no selection in trace mode)
+    const size_t smem = MODE == rtk::kTrace ? 0 : (size_t)(kThreads / 32) * 32 * E * 8;
+    if (a.m == 32 * E) return launch_rows(rtk::rowtopk_kernel<MODE, rtk::LaneRow<E, false>>, a, s, smem);
+    return launch_rows(rtk::rowtopk_kernel<MODE, rtk::LaneRow<E, true>>, a, s, smem);
+}
+
 template <int MODE>
 int dispatch(const rtk::Args& a, cudaStream_t s) {
     const int m = a.m;
     const bool vec4 = (m % 4 == 0) && (a.ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
     if (m <= 1024 && vec4) {
+        // elements per lane: ceil(m / 32) rounded up to a multiple of 4
         switch ((m + 127) / 128) {
-            case 1: return launch_reg<MODE, 4, 1>(a, s);
-            case 2: return launch_reg<MODE, 4, 2>(a, s);
-            case 3: return launch_reg<MODE, 4, 3>(a, s);
-            case 4: return launch_reg<MODE, 4, 4>(a, s);
-            case 5: return launch_reg<MODE, 4, 5>(a, s);
-            case 6: return launch_reg<MODE, 4, 6>(a, s);
-            case 7: return launch_reg<MODE, 4, 7>(a, s);
-            default: return launch_reg<MODE, 4, 8>(a, s);
+            case 1: return launch_lane<MODE, 4>(a, s);
+            case 2: return launch_lane<MODE, 8>(a, s);
+            case 3: return launch_lane<MODE, 12>(a, s);
+            case 4: return launch_lane<MODE, 16>(a, s);
+            case 5: return launch_lane<MODE, 20>(a, s);
+            case 6: return launch_lane<MODE, 24>(a, s);
+            case 7: return launch_lane<MODE, 28>(a, s);
+            default: return launch_lane<MODE, 32>(a, s);
         }
     }
     if (m <= 1024) {

@@ -151,6 +151,7 @@ __device__ __forceinline__ unsigned warp_incl_scan(unsigned x) {
 template <int V, int C, bool MASKED>
 struct RegRow {
     static constexpr bool kStaged = true;  // selection goes through shared memory
+    static constexpr int kPad = 0;         // staging holds exactly k entries
     static constexpr int kV = V;
     static constexpr int kC = C;
     float v[C][V];
@@ -195,6 +196,8 @@ struct RegRow {
     }
 
     // Biased lane count of v >= t (see kLaneBias): FSET.BF + FADD2 per pair.
+    __device__ __forceinline__ static int lane_valid(int, int) { return 0; }  // unused (no hint)
+
     __device__ __forceinline__ int lane_count_ge(float t) const {
         constexpr int kSlots = C * V;
         float sx = __int_as_float((int)kLaneBias), sy = 0.0f;
@@ -212,7 +215,7 @@ struct RegRow {
 
     // Stage the first k elements (ascending index) with v >= t into the
     // warp's shared-memory row buffer (_kernels.py:118-125, 205-212).
-    __device__ __forceinline__ void select_ge(float t, int k, unsigned sbase, int lane) const {
+    __device__ __forceinline__ void select_ge(float t, int k, unsigned sbase, int lane, int) const {
         bool p[C][V];
 #pragma unroll
         for (int c = 0; c < C; ++c)
@@ -303,6 +306,7 @@ struct RegRow {
 __device__ __forceinline__ void flush_row(unsigned sbase, int k, float* __restrict__ ov, int* __restrict__ oi,
                                           int lane) {
     __syncwarp();
+#pragma unroll 1
     for (int j = lane; j < k; j += 32) {
         float v;
         int i;
@@ -313,12 +317,121 @@ __device__ __forceinline__ void flush_row(unsigned sbase, int k, float* __restri
     __syncwarp();
 }
 
+// ------------------------------------------------- lane-contiguous row tile
+//
+// The register layout of the vectorised path: lane l holds the E consecutive
+// elements [l*E, l*E + E) of the row (E a multiple of 4, E*32 >= M), loaded
+// with 256-bit LDG.E.256 (E % 8 == 0, unmasked) or 128-bit loads.  Index order
+// is (lane, slot), so one warp exclusive scan of the per-lane hit counts gives
+// every selected element its output position.  Padding slots hold NaN.
+template <int E, bool MASKED>
+struct LaneRow {
+    static constexpr bool kStaged = true;
+    static constexpr int kSlots = E;
+    static constexpr int kPad = 32 * E;  // staging entries per warp
+    float v[E];
+
+    __device__ __forceinline__ static bool valid(int lane, int q, int m) { return !MASKED || lane * E + q < m; }
+
+    __device__ __forceinline__ void load(const float* __restrict__ p, int m, int lane) {
+        const float* lp = p + lane * E;
+        if constexpr (!MASKED && E % 8 == 0) {
+#pragma unroll
+            for (int g = 0; g < E / 8; ++g) {
+                float* d = v + 8 * g;
+                asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                             : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3]), "=f"(d[4]), "=f"(d[5]), "=f"(d[6]),
+                               "=f"(d[7])
+                             : "l"(lp + 8 * g));
+            }
+        } else {
+#pragma unroll
+            for (int g = 0; g < E / 4; ++g) {
+                if (valid(lane, 4 * g, m)) {
+                    const float4 q = ld_stream4(lp + 4 * g);
+                    v[4 * g] = q.x; v[4 * g + 1] = q.y; v[4 * g + 2] = q.z; v[4 * g + 3] = q.w;
+                } else {
+                    v[4 * g] = v[4 * g + 1] = v[4 * g + 2] = v[4 * g + 3] = __int_as_float(0x7fffffff);
+                }
+            }
+        }
+    }
+
+    __device__ __forceinline__ void lane_min_max(int m, int lane, float& mn, float& mx) const {
+        mn = __int_as_float(0x7f800000);
+        mx = __int_as_float(0xff800000);
+#pragma unroll
+        for (int q = 0; q < E; ++q) {
+            if (valid(lane, q, m)) mn = fmin_nan(mn, v[q]);
+            mx = fmaxf(mx, v[q]);
+        }
+    }
+
+    __device__ __forceinline__ int lane_count_ge(float t) const {
+        float sx = set_ge(v[0], t), sy = set_ge(v[1], t);
+#pragma unroll
+        for (int q = 2; q < E; q += 2) add2(sx, sy, set_ge(v[q], t), set_ge(v[q + 1], t));
+        return __float_as_int(__fadd_rn(__fadd_rn(sx, sy), 0x1p23f));  // kLaneBias + count
+    }
+
+    // Number of real (non-padding) slots of this lane.
+    __device__ __forceinline__ static int lane_valid(int m, int lane) {
+        return MASKED ? max(0, min(E, m - lane * E)) : E;
+    }
+
+    // Stage every element with v >= t at its output position (the caller
+    // guarantees #{v >= t} >= k and flushes only the first k entries; the
+    // staging buffer holds kPad entries, so no per-element cutoff is needed).
+    // lane_hits: #{v >= t} in this lane, already known from the search pass
+    // at t (the lane input of that pass's REDUX).
+    __device__ __forceinline__ void select_ge(float t, int, unsigned sbase, int lane, int lane_hits) const {
+        const unsigned cl = (unsigned)lane_hits;
+        const unsigned excl = warp_incl_scan(cl) - cl;
+        unsigned addr = sbase + 8u * excl;
+        const int i0 = lane * E;
+#pragma unroll
+        for (int q = 0; q < E; ++q) {
+            if (v[q] >= t) {
+                stage_put(addr, v[q], i0 + q);
+                addr += 8u;
+            }
+        }
+    }
+
+    // All v >= t plus the first `need` elements of [lo, t), ascending index
+    // (_kernels.py:126-145).  Cold on benchmark data.
+    __device__ __forceinline__ void select_fill(float t, float lo, int need, int, unsigned sbase, int lane) const {
+        bool pa[E], pb[E];
+        unsigned packed = 0;
+#pragma unroll
+        for (int q = 0; q < E; ++q) {
+            pa[q] = v[q] >= t;
+            pb[q] = (lo <= v[q]) && (v[q] < t);
+            packed += (pa[q] ? 1u : 0u) + (pb[q] ? 0x10000u : 0u);
+        }
+        const unsigned excl = warp_incl_scan(packed) - packed;
+        int ea = (int)(excl & 0xffffu), eb = (int)(excl >> 16);
+        const int i0 = lane * E;
+#pragma unroll
+        for (int q = 0; q < E; ++q) {
+            if (pa[q]) {
+                stage_put(sbase + 8u * (ea + min(eb, need)), v[q], i0 + q);
+                ++ea;
+            } else if (pb[q]) {
+                if (eb < need) stage_put(sbase + 8u * (ea + eb), v[q], i0 + q);
+                ++eb;
+            }
+        }
+    }
+};
+
 // ------------------------------------------------------ global-memory row
 //
 // Rows longer than the register tile: same layout with V = 1 and a runtime
 // chunk count, every pass re-reading the row (L1/L2 resident after pass 1).
 struct GlobalRow {
     static constexpr bool kStaged = false;  // selection stores straight to global
+    static constexpr int kPad = 0;
     const float* __restrict__ p;
     int m;
 
@@ -337,13 +450,15 @@ struct GlobalRow {
             mx = fmaxf(mx, x);
         }
     }
+    __device__ __forceinline__ static int lane_valid(int, int) { return 0; }  // unused (no hint)
+
     __device__ __forceinline__ int lane_count_ge(float t) const {
         int cnt = 0;
         for (int e = threadIdx.x & 31; e < m; e += 32) cnt += (__ldg(p + e) >= t) ? 1 : 0;
         return (int)kLaneBias + cnt;
     }
     __device__ __forceinline__ void select_ge(float t, int k, float* __restrict__ ov, int* __restrict__ oi,
-                                              int lane) const {
+                                              int lane, int) const {
         int base = 0;
         const unsigned lt = lanemask_lt();
         for (int c0 = 0; c0 < m && base < k; c0 += 32) {
@@ -398,29 +513,66 @@ struct GlobalRow {
 // SAFE: |mn0|,|mx0| < 2^126 so the midpoint cannot overflow.
 // cnt is returned biased by kCountBias.
 template <bool FP, bool SAFE, class Row>
-__device__ __forceinline__ int exact_loop(const Row& row, int kb, double eps, int hard_cap, float& mn, float& mx,
-                                          float& thres, int& cnt, int& it) {
-    // One body per bisection step with a single exit branch.  The bracket
-    // update is applied unconditionally: on a no-progress exit (mid equal to
-    // the bound being replaced) it is a no-op, and on cnt == k the moved
-    // lower bound is never read again (select_exact uses thres and cnt).
-    bool eq, stuck, cont;
+__device__ __forceinline__ int exact_loop(const Row& row, int kb, double eps, int cap, float& mn, float& mx,
+                                          float& thres, int& cnt, int& it, int& lane_last) {
     float mid;
-    do {
-        ++it;
-        mid = SAFE ? mid_fast(mn, mx) : mid_exact(mn, mx);
-        cnt = warp_count(row.lane_count_ge(mid));
-        const bool lt = cnt < kb;
-        eq = cnt == kb;
-        stuck = mid == (lt ? mx : mn);
+    if constexpr (FP && SAFE) {
+        // mid = RN((mn+mx)/2) always lies in [mn, mx].  If it is strictly
+        // inside, neither no-progress exit can fire and the updated bracket
+        // still satisfies mx > mn; if it equals an endpoint the reference
+        // exits after this body with INTERVAL_BELOW_EPSILON (stuck, or the
+        // bracket collapses and the next head test fails) unless cnt == k.
+        bool eq, inside;
+        do {
+            ++it;
+            mid = mid_fast(mn, mx);
+            inside = (mn < mid) && (mid < mx);
+            lane_last = row.lane_count_ge(mid);
+            cnt = warp_count(lane_last);
+            const bool lt = cnt < kb;
+            eq = cnt == kb;
+            mx = lt ? mid : mx;
+            mn = lt ? mn : mid;
+        } while (!eq && inside && it < cap);
+        thres = mid;
+        if (eq) return kExitCountEqualsK;
+        return inside ? kExitHardCapReached : kExitIntervalBelowEps;
+    } else {
+        // General form: explicit no-progress tests and the float64 head test
+        // (_kernels.py:65,78,82).  The bracket update is applied
+        // unconditionally: on a no-progress exit it is a no-op.
+        bool eq, stuck, cont;
+        do {
+            ++it;
+            mid = SAFE ? mid_fast(mn, mx) : mid_exact(mn, mx);
+            lane_last = row.lane_count_ge(mid);
+            cnt = warp_count(lane_last);
+            const bool lt = cnt < kb;
+            eq = cnt == kb;
+            stuck = mid == (lt ? mx : mn);
+            mx = lt ? mid : mx;
+            mn = lt ? mn : mid;
+            cont = FP ? (mx > mn) : ((double)mx - (double)mn > eps);
+        } while (!eq && !stuck && cont && it < cap);
+        thres = mid;
+        if (eq) return kExitCountEqualsK;
+        if (stuck || !cont) return kExitIntervalBelowEps;
+        return kExitHardCapReached;
+    }
+}
+
+// Algorithm 2 loop (_kernels.py:96-102): exactly max_iter steps; also tracks
+// this lane's count at the final lower bound (the selection threshold).
+template <bool SAFE, class Row>
+__device__ __forceinline__ void early_loop(const Row& row, int kb, int max_iter, float& mn, float& mx, int& lane_mn) {
+    for (int i = 0; i < max_iter; ++i) {
+        const float mid = SAFE ? mid_fast(mn, mx) : mid_exact(mn, mx);
+        const int lc = row.lane_count_ge(mid);
+        const bool lt = warp_count(lc) < kb;
         mx = lt ? mid : mx;
         mn = lt ? mn : mid;
-        cont = FP ? (mx > mn) : ((double)mx - (double)mn > eps);
-    } while (!eq && !stuck && cont && it < hard_cap);
-    thres = mid;
-    if (eq) return kExitCountEqualsK;
-    if (stuck || !cont) return kExitIntervalBelowEps;
-    return kExitHardCapReached;
+        lane_mn = lt ? lane_mn : lc;
+    }
 }
 
 template <int MODE, class Row>
@@ -436,71 +588,68 @@ __device__ __forceinline__ void process_row(const Row& row, long long r, const A
     float* ov = a.vals + r * a.ldo;
     int* oi = a.idx + r * a.ldo;
     int it = 0, reason;
+    const bool safe = fabsf(mn0) < 0x1p126f && fabsf(mx0) < 0x1p126f;
 
     if constexpr (MODE == kEarly) {
         // Algorithm 2 (_kernels.py:87-103) + first-k selection (:205-212)
         float mn = mn0, mx = mx0;
+        int lane_mn = (int)kLaneBias + Row::lane_valid(a.m, lane);  // every element is >= mn0
         if (!(mx0 > mn0)) {
             reason = kExitDegenerateRow;
         } else {
-            const int max_iter = a.max_iter;
-            if (fabsf(mn0) < 0x1p126f && fabsf(mx0) < 0x1p126f) {
-                for (int i = 0; i < max_iter; ++i) {
-                    const float mid = mid_fast(mn, mx);
-                    const bool lt = warp_count(row.lane_count_ge(mid)) < kb;
-                    mx = lt ? mid : mx;
-                    mn = lt ? mn : mid;
-                }
-            } else {
-                for (int i = 0; i < max_iter; ++i) {
-                    const float mid = mid_exact(mn, mx);
-                    const bool lt = warp_count(row.lane_count_ge(mid)) < kb;
-                    mx = lt ? mid : mx;
-                    mn = lt ? mn : mid;
-                }
-            }
-            it = max_iter;
+            if (safe)
+                early_loop<true>(row, kb, a.max_iter, mn, mx, lane_mn);
+            else
+                early_loop<false>(row, kb, a.max_iter, mn, mx, lane_mn);
+            it = a.max_iter;
             reason = kExitMaxIterReached;
         }
         if constexpr (Row::kStaged) {
-            row.select_ge(mn, k, sbase, lane);
+            row.select_ge(mn, k, sbase, lane, lane_mn - (int)kLaneBias);
             flush_row(sbase, k, ov, oi, lane);
         } else {
-            row.select_ge(mn, k, ov, oi, lane);
+            row.select_ge(mn, k, ov, oi, lane, 0);
         }
     } else {
         // Algorithm 1 (_kernels.py:48-84) + select_exact (_kernels.py:149-162)
         const bool fp = (a.eps_rel == 0.0);
         float mn = mn0, mx = mx0, thres = mn0;
         int cnt = a.m + kCountBias;
+        int lane_t = (int)kLaneBias + Row::lane_valid(a.m, lane);  // lane count at thres
+        const int cap = a.hard_cap;
         if (fp) {
             if (!(isfinite(mx0) && mx0 > mn0)) {
                 reason = kExitDegenerateRow;  // eps = 0*mx0 is NaN for infinite mx0
-            } else if (fabsf(mn0) < 0x1p126f && fabsf(mx0) < 0x1p126f) {
-                reason = exact_loop<true, true>(row, kb, 0.0, a.hard_cap, mn, mx, thres, cnt, it);
+            } else if (safe) {
+                reason = exact_loop<true, true>(row, kb, 0.0, cap, mn, mx, thres, cnt, it, lane_t);
             } else {
-                reason = exact_loop<true, false>(row, kb, 0.0, a.hard_cap, mn, mx, thres, cnt, it);
+                reason = exact_loop<true, false>(row, kb, 0.0, cap, mn, mx, thres, cnt, it, lane_t);
             }
         } else {
             const double eps = a.eps_rel * (double)mx0;
             if (!((double)mx0 - (double)mn0 > eps))
                 reason = kExitDegenerateRow;
             else
-                reason = exact_loop<false, false>(row, kb, eps, a.hard_cap, mn, mx, thres, cnt, it);
+                reason = exact_loop<false, false>(row, kb, eps, cap, mn, mx, thres, cnt, it, lane_t);
         }
         if constexpr (MODE == kExact) {
             const bool use_mx = (cnt > kb) && fp && (reason != kExitDegenerateRow);
-            const float t = use_mx ? mx : thres;
-            const int ca = (use_mx ? warp_count(row.lane_count_ge(mx)) : cnt) - kCountBias;
+            float t = thres;
+            int ca = cnt - kCountBias;
+            if (use_mx) {
+                t = mx;
+                lane_t = row.lane_count_ge(mx);
+                ca = warp_count(lane_t) - kCountBias;
+            }
             if constexpr (Row::kStaged) {
                 if (ca >= k)
-                    row.select_ge(t, k, sbase, lane);
+                    row.select_ge(t, k, sbase, lane, lane_t - (int)kLaneBias);
                 else
                     row.select_fill(t, mn, k - ca, k, sbase, lane);
                 flush_row(sbase, k, ov, oi, lane);
             } else {
                 if (ca >= k)
-                    row.select_ge(t, k, ov, oi, lane);
+                    row.select_ge(t, k, ov, oi, lane, 0);
                 else
                     row.select_fill(t, mn, k - ca, k, ov, oi, lane);
             }
@@ -519,9 +668,14 @@ template <int MODE, class Row>
 __global__ void __launch_bounds__(256) rowtopk_kernel(Args a) {
     extern __shared__ __align__(16) float smem[];
     const int lane = threadIdx.x & 31;
-    const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem) + (threadIdx.x >> 5) * 8u * a.k;
+    const unsigned per_warp = Row::kPad ? (unsigned)Row::kPad : (unsigned)a.k;  // staging entries
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem) + (threadIdx.x >> 5) * 8u * per_warp;
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-    long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    // The warp index is broadcast from lane 0 so ptxas can prove every row
+    // loop below warp-uniform (no BRA.DIV convergence checks before the
+    // REDUX/SHFL collectives, and uniform registers for the row bookkeeping).
+    const int wid = __shfl_sync(kFull, (int)(threadIdx.x >> 5), 0);
+    long long r = (long long)blockIdx.x * (blockDim.x >> 5) + wid;
     if (r >= a.n) return;
     Row A, B;
     A.load(a.x + r * a.ldx, a.m, lane);
