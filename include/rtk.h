@@ -25,8 +25,9 @@
  * row r start at vals + r*ldo / idx + r*ldo (ldo >= k).  Exactly k values and
  * k int32 indices are written per row, indices ascending, values bit copies
  * of x (_kernels.py:106-146).  iters (int32) / reasons (int8, ExitReason codes
- * 1..5, _kernels.py:19-23) are per-row traces and may be NULL (trace
- * collection off, BatchConfig.collect_traces=False, batch.py:58).
+ * 1..5, _kernels.py:19-23) are per-row traces; both NULL turns trace
+ * collection off (BatchConfig.collect_traces=False, batch.py:58), exactly one
+ * NULL is RTK_EINVAL.
  *
  * Return value: RTK_OK, RTK_EINVAL (bad sizes, k not in [1, m], NULL
  * required pointer), or RTK_ECUDA (launch failure); rtk_last_error() then

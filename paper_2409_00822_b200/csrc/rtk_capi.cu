@@ -82,20 +82,36 @@ int launch_rows(K kernel, const rtk::Args& a, cudaStream_t s, size_t smem) {
     return RTK_OK;
 }
 
+// Launch one row-kernel instantiation; traces are a template flag so the
+// common no-trace launch carries no per-row trace stores.
+template <int MODE, class Row>
+int launch_row_kernel(const rtk::Args& a, cudaStream_t s, size_t smem) {
+    if constexpr (MODE == rtk::kTrace) {
+        return launch_rows(rtk::rowtopk_kernel<MODE, Row, true>, a, s, smem);
+    } else {
+        if ((a.iters != nullptr) != (a.reasons != nullptr))
+            return fail(RTK_EINVAL, "iters and reasons must be both NULL or both non-NULL");
+        if (a.iters != nullptr) return launch_rows(rtk::rowtopk_kernel<MODE, Row, true>, a, s, smem);
+        return launch_rows(rtk::rowtopk_kernel<MODE, Row, false>, a, s, smem);
+    }
+}
+
 template <int MODE, int V, int C>
 int launch_reg(const rtk::Args& a, cudaStream_t s) {
-    // staging buffer: k values + k indices per warp (no selection in trace mode)
+    // staging buffer: k (value, index) pairs per warp (no selection in trace mode)
     const size_t smem = MODE == rtk::kTrace ? 0 : (size_t)(kThreads / 32) * 2 * a.k * sizeof(float);
-    if (a.m == C * 32 * V) return launch_rows(rtk::rowtopk_kernel<MODE, rtk::RegRow<V, C, false>>, a, s, smem);
-    return launch_rows(rtk::rowtopk_kernel<MODE, rtk::RegRow<V, C, true>>, a, s, smem);
+    if (a.m == C * 32 * V) return launch_row_kernel<MODE, rtk::RegRow<V, C, false>>(a, s, smem);
+    return launch_row_kernel<MODE, rtk::RegRow<V, C, true>>(a, s, smem);
 }
 
 template <int MODE, int E>
 int launch_lane(const rtk::Args& a, cudaStream_t s) {
     // staging buffer: 32*E (value, index) pairs per warp (no selection in trace mode)
     const size_t smem = MODE == rtk::kTrace ? 0 : (size_t)(kThreads / 32) * 32 * E * 8;
-    if (a.m == 32 * E) return launch_rows(rtk::rowtopk_kernel<MODE, rtk::LaneRow<E, false>>, a, s, smem);
-    return launch_rows(rtk::rowtopk_kernel<MODE, rtk::LaneRow<E, true>>, a, s, smem);
+    const bool wide = (reinterpret_cast<uintptr_t>(a.x) & 31) == 0 && a.ldx % 8 == 0;  // 256-bit loads
+    if (a.m == 32 * E && wide) return launch_row_kernel<MODE, rtk::LaneRow<E, false, true>>(a, s, smem);
+    if (a.m == 32 * E) return launch_row_kernel<MODE, rtk::LaneRow<E, false, false>>(a, s, smem);
+    return launch_row_kernel<MODE, rtk::LaneRow<E, true, false>>(a, s, smem);
 }
 
 template <int MODE>
@@ -124,7 +140,7 @@ int dispatch(const rtk::Args& a, cudaStream_t s) {
         if (c <= 16) return launch_reg<MODE, 1, 16>(a, s);
         return launch_reg<MODE, 1, 32>(a, s);
     }
-    return launch_rows(rtk::rowtopk_kernel<MODE, rtk::GlobalRow>, a, s, 0);
+    return launch_row_kernel<MODE, rtk::GlobalRow>(a, s, 0);
 }
 
 int launch_flat(void (*kernel)(rtk::Args), const rtk::Args& a, cudaStream_t s) {

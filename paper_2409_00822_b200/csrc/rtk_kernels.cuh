@@ -321,10 +321,11 @@ __device__ __forceinline__ void flush_row(unsigned sbase, int k, float* __restri
 //
 // The register layout of the vectorised path: lane l holds the E consecutive
 // elements [l*E, l*E + E) of the row (E a multiple of 4, E*32 >= M), loaded
-// with 256-bit LDG.E.256 (E % 8 == 0, unmasked) or 128-bit loads.  Index order
+// with 256-bit LDG.E.256 (WIDE: E % 8 == 0, unmasked, 32-byte aligned rows)
+// or 128-bit loads.  Index order
 // is (lane, slot), so one warp exclusive scan of the per-lane hit counts gives
 // every selected element its output position.  Padding slots hold NaN.
-template <int E, bool MASKED>
+template <int E, bool MASKED, bool WIDE = false>
 struct LaneRow {
     static constexpr bool kStaged = true;
     static constexpr int kSlots = E;
@@ -335,7 +336,7 @@ struct LaneRow {
 
     __device__ __forceinline__ void load(const float* __restrict__ p, int m, int lane) {
         const float* lp = p + lane * E;
-        if constexpr (!MASKED && E % 8 == 0) {
+        if constexpr (WIDE && !MASKED && E % 8 == 0) {
 #pragma unroll
             for (int g = 0; g < E / 8; ++g) {
                 float* d = v + 8 * g;
@@ -512,6 +513,16 @@ struct GlobalRow {
 // each body (before the next body's hard-cap test, the reference order).
 // SAFE: |mn0|,|mx0| < 2^126 so the midpoint cannot overflow.
 // cnt is returned biased by kCountBias.
+// Per-row output cursor: advanced by a fixed stride per grid step instead of
+// recomputing 64-bit row offsets.
+struct RowOut {
+    float* __restrict__ ov;
+    int* __restrict__ oi;
+    int* __restrict__ it;
+    signed char* __restrict__ rs;
+    long long r;
+};
+
 template <bool FP, bool SAFE, class Row>
 __device__ __forceinline__ int exact_loop(const Row& row, int kb, double eps, int cap, float& mn, float& mx,
                                           float& thres, int& cnt, int& it, int& lane_last) {
@@ -575,8 +586,9 @@ __device__ __forceinline__ void early_loop(const Row& row, int kb, int max_iter,
     }
 }
 
-template <int MODE, class Row>
-__device__ __forceinline__ void process_row(const Row& row, long long r, const Args& a, int lane, unsigned sbase) {
+template <int MODE, bool TRACES, class Row>
+__device__ __forceinline__ void process_row(const Row& row, const RowOut& o, const Args& a, int lane, unsigned sbase) {
+    const long long r = o.r;
     float mnl, mxl;
     row.lane_min_max(a.m, lane, mnl, mxl);
     const float mn0 = warp_min_nan(mnl), mx0 = warp_max(mxl);
@@ -585,8 +597,8 @@ __device__ __forceinline__ void process_row(const Row& row, long long r, const A
     }
     const int k = a.k;
     const int kb = k + kCountBias;
-    float* ov = a.vals + r * a.ldo;
-    int* oi = a.idx + r * a.ldo;
+    float* ov = o.ov;
+    int* oi = o.oi;
     int it = 0, reason;
     const bool safe = fabsf(mn0) < 0x1p126f && fabsf(mx0) < 0x1p126f;
 
@@ -655,40 +667,50 @@ __device__ __forceinline__ void process_row(const Row& row, long long r, const A
             }
         }
     }
-    if (lane == 0) {
-        if (a.iters) a.iters[r] = it;
-        if (a.reasons) a.reasons[r] = (signed char)reason;
+    if constexpr (TRACES) {
+        if (lane == 0) {
+            *o.it = it;
+            *o.rs = (signed char)reason;
+        }
     }
 }
 
 // Persistent grid-stride row loop; each warp prefetches its next row into a
-// second register tile while the current one is searched.  Dynamic shared
-// memory: one k-value + k-index staging buffer per warp (staged rows only).
-template <int MODE, class Row>
+// second register tile while the current one is searched (the prefetch is
+// unconditional -- past the last row it re-reads the current row -- so no
+// predicated register copies sit behind the load).  Dynamic shared memory:
+// one staging buffer of (value, index) pairs per warp (staged rows only).
+template <int MODE, class Row, bool TRACES>
 __global__ void __launch_bounds__(256) rowtopk_kernel(Args a) {
     extern __shared__ __align__(16) float smem[];
     const int lane = threadIdx.x & 31;
     const unsigned per_warp = Row::kPad ? (unsigned)Row::kPad : (unsigned)a.k;  // staging entries
-    const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem) + (threadIdx.x >> 5) * 8u * per_warp;
-    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
     // The warp index is broadcast from lane 0 so ptxas can prove every row
     // loop below warp-uniform (no BRA.DIV convergence checks before the
     // REDUX/SHFL collectives, and uniform registers for the row bookkeeping).
     const int wid = __shfl_sync(kFull, (int)(threadIdx.x >> 5), 0);
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem) + (unsigned)wid * 8u * per_warp;
+    const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
     long long r = (long long)blockIdx.x * (blockDim.x >> 5) + wid;
     if (r >= a.n) return;
+    const long long xstep = nw * a.ldx, ostep = nw * a.ldo;
+    const float* xp = a.x + r * a.ldx;
+    RowOut o{a.vals + r * a.ldo, a.idx + r * a.ldo, a.iters + r, a.reasons + r, r};
     Row A, B;
-    A.load(a.x + r * a.ldx, a.m, lane);
+    A.load(xp, a.m, lane);
     for (;;) {
-        const long long r1 = r + nw;
-        if (r1 < a.n) B.load(a.x + r1 * a.ldx, a.m, lane);
-        process_row<MODE>(A, r, a, lane, sbase);
-        if (r1 >= a.n) break;
-        const long long r2 = r1 + nw;
-        if (r2 < a.n) A.load(a.x + r2 * a.ldx, a.m, lane);
-        process_row<MODE>(B, r1, a, lane, sbase);
-        if (r2 >= a.n) break;
-        r = r2;
+        const bool more1 = o.r + nw < a.n;
+        xp += more1 ? xstep : 0;
+        B.load(xp, a.m, lane);
+        process_row<MODE, TRACES>(A, o, a, lane, sbase);
+        if (!more1) break;
+        o.r += nw; o.ov += ostep; o.oi += ostep; o.it += nw; o.rs += nw;
+        const bool more2 = o.r + nw < a.n;
+        xp += more2 ? xstep : 0;
+        A.load(xp, a.m, lane);
+        process_row<MODE, TRACES>(B, o, a, lane, sbase);
+        if (!more2) break;
+        o.r += nw; o.ov += ostep; o.oi += ostep; o.it += nw; o.rs += nw;
     }
 }
 
