@@ -34,6 +34,10 @@ constexpr unsigned kFull = 0xffffffffu;
 
 enum Mode : int { kExact = 0, kEarly = 1, kTrace = 2 };
 
+#ifndef RTK_MIN_CTAS
+#define RTK_MIN_CTAS 1  // __launch_bounds__ min CTAs per SM for the row kernels
+#endif
+
 struct Args {
     const float* __restrict__ x;
     long long n;
@@ -111,6 +115,7 @@ __device__ __forceinline__ float4 ld_stream4(const float* p) {
     return __ldcs(reinterpret_cast<const float4*>(p));
 }
 __device__ __forceinline__ float ld_stream1(const float* p) { return __ldcs(p); }
+
 
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned r;
@@ -681,7 +686,7 @@ __device__ __forceinline__ void process_row(const Row& row, const RowOut& o, con
 // predicated register copies sit behind the load).  Dynamic shared memory:
 // one staging buffer of (value, index) pairs per warp (staged rows only).
 template <int MODE, class Row, bool TRACES>
-__global__ void __launch_bounds__(256) rowtopk_kernel(Args a) {
+__global__ void __launch_bounds__(256, RTK_MIN_CTAS) rowtopk_kernel(Args a) {
     extern __shared__ __align__(16) float smem[];
     const int lane = threadIdx.x & 31;
     const unsigned per_warp = Row::kPad ? (unsigned)Row::kPad : (unsigned)a.k;  // staging entries

@@ -1,0 +1,10 @@
+#!/bin/bash
+# Benchmark prebuilt librtk variants: bash tools/gpu_sweep.sh TAG lib1.so lib2.so ...
+TAG=$1; shift
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+for LIB in "$@"; do
+  name=$(basename $LIB .so)
+  RTK_LIBRARY=$LIB timeout 300 python bench.py --no-cpu --no-e2e --no-torch --steps 300 > $OUT/$name.json 2> $OUT/$name.err
+done
+echo done > $OUT/DONE
