@@ -27,7 +27,8 @@ int fail(int code, const char* fmt, ...) {
     return code;
 }
 
-constexpr int kThreads = 256;  // 8 warps per CTA
+constexpr int kThreads = RTK_CTA_THREADS;  // threads per CTA of the row kernels
+constexpr int kFlatThreads = 256;         // threads per CTA of the elementwise kernels
 constexpr int kMaxDevices = 64;
 
 struct DeviceInfo {
@@ -104,8 +105,26 @@ int launch_reg(const rtk::Args& a, cudaStream_t s) {
     return launch_row_kernel<MODE, rtk::RegRow<V, C, true>>(a, s, smem);
 }
 
+template <int MODE, class Row>
+int launch_pipe_kernel(const rtk::Args& a, cudaStream_t s) {
+    // per warp: selection staging (kPad pairs) + RTK_PIPE_DEPTH row slots
+    const size_t smem = (size_t)(kThreads / 32) * (8 * Row::kPad + RTK_PIPE_DEPTH * Row::kRowBytes);
+    if constexpr (MODE == rtk::kTrace) {
+        return launch_rows(rtk::rowtopk_pipe_kernel<MODE, Row, true>, a, s, smem);
+    } else {
+        if ((a.iters != nullptr) != (a.reasons != nullptr))
+            return fail(RTK_EINVAL, "iters and reasons must be both NULL or both non-NULL");
+        if (a.iters != nullptr) return launch_rows(rtk::rowtopk_pipe_kernel<MODE, Row, true>, a, s, smem);
+        return launch_rows(rtk::rowtopk_pipe_kernel<MODE, Row, false>, a, s, smem);
+    }
+}
+
 template <int MODE, int E>
 int launch_lane(const rtk::Args& a, cudaStream_t s) {
+#ifndef RTK_NO_PIPE
+    if (a.m == 32 * E) return launch_pipe_kernel<MODE, rtk::LaneRow<E, false, false>>(a, s);
+    return launch_pipe_kernel<MODE, rtk::LaneRow<E, true, false>>(a, s);
+#endif
     // staging buffer: 32*E (value, index) pairs per warp (no selection in trace mode)
     const size_t smem = MODE == rtk::kTrace ? 0 : (size_t)(kThreads / 32) * 32 * E * 8;
     const bool wide = (reinterpret_cast<uintptr_t>(a.x) & 31) == 0 && a.ldx % 8 == 0;  // 256-bit loads
@@ -145,11 +164,11 @@ int dispatch(const rtk::Args& a, cudaStream_t s) {
 
 int launch_flat(void (*kernel)(rtk::Args), const rtk::Args& a, cudaStream_t s) {
     const long long total = a.n * (long long)a.m;
-    long long grid = (total + kThreads - 1) / kThreads;
+    long long grid = (total + kFlatThreads - 1) / kFlatThreads;
     const long long cap = (long long)device_sms() * 8;
     if (grid > cap) grid = cap;
     if (grid < 1) grid = 1;
-    kernel<<<(unsigned)grid, kThreads, 0, s>>>(a);
+    kernel<<<(unsigned)grid, kFlatThreads, 0, s>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(RTK_ECUDA, "kernel launch failed: %s", cudaGetErrorString(e));
     return RTK_OK;
@@ -269,7 +288,7 @@ int rtk_row_min_max_f32(const float* x, int64_t n, int64_t m, int64_t ldx, float
     rtk::Args a = make_args(x, n, m, ldx, 1, nullptr, nullptr, 1, nullptr, nullptr, nullptr);
     long long grid = (n + 7) / 8, cap = (long long)device_sms() * 8;
     if (grid > cap) grid = cap;
-    rtk::min_max_kernel<<<(unsigned)grid, kThreads, 0, s>>>(a, mins, maxs);
+    rtk::min_max_kernel<<<(unsigned)grid, kFlatThreads, 0, s>>>(a, mins, maxs);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(RTK_ECUDA, "kernel launch failed: %s", cudaGetErrorString(e));
     return RTK_OK;
@@ -285,7 +304,7 @@ int rtk_count_ge_f32(const float* x, int64_t n, int64_t m, int64_t ldx, const fl
     rtk::Args a = make_args(x, n, m, ldx, 1, nullptr, nullptr, 1, nullptr, nullptr, nullptr);
     long long grid = (n + 7) / 8, cap = (long long)device_sms() * 8;
     if (grid > cap) grid = cap;
-    rtk::count_ge_kernel<<<(unsigned)grid, kThreads, 0, s>>>(a, thres, counts);
+    rtk::count_ge_kernel<<<(unsigned)grid, kFlatThreads, 0, s>>>(a, thres, counts);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(RTK_ECUDA, "kernel launch failed: %s", cudaGetErrorString(e));
     return RTK_OK;

@@ -37,6 +37,9 @@ enum Mode : int { kExact = 0, kEarly = 1, kTrace = 2 };
 #ifndef RTK_MIN_CTAS
 #define RTK_MIN_CTAS 1  // __launch_bounds__ min CTAs per SM for the row kernels
 #endif
+#ifndef RTK_CTA_THREADS
+#define RTK_CTA_THREADS 256  // threads per CTA of the row kernels
+#endif
 
 struct Args {
     const float* __restrict__ x;
@@ -120,6 +123,20 @@ __device__ __forceinline__ float ld_stream1(const float* p) { return __ldcs(p); 
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned r;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+
+// Asynchronous global -> shared copies (LDGSTS), 16 bytes each; src_bytes = 0
+// zero-fills (padding groups).  Bypass L1 (.cg): each byte is read once.
+__device__ __forceinline__ void cp_async16(unsigned dst, const void* src, unsigned src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ float4 lds128(unsigned addr) {
+    float4 r;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "r"(addr) : "memory");
     return r;
 }
 
@@ -363,6 +380,32 @@ struct LaneRow {
         }
     }
 
+    // Row bytes of one pipeline slot (a warp's copy of one row).
+    static constexpr unsigned kRowBytes = 32u * E * 4u;
+
+    // Issue this lane's share of row p into shared slot `slot` (every lane
+    // later reads back exactly the bytes it copied, so no cross-lane sync).
+    __device__ __forceinline__ static void stage_async(const float* __restrict__ p, int m, int lane, unsigned slot) {
+        const float* lp = p + lane * E;
+        const unsigned dst = slot + (unsigned)lane * E * 4u;
+#pragma unroll
+        for (int g = 0; g < E / 4; ++g) cp_async16(dst + 16u * g, lp + 4 * g, valid(lane, 4 * g, m) ? 16u : 0u);
+    }
+
+    __device__ __forceinline__ void load_smem(unsigned slot, int m, int lane) {
+        const unsigned src = slot + (unsigned)lane * E * 4u;
+#pragma unroll
+        for (int g = 0; g < E / 4; ++g) {
+            const float4 q = lds128(src + 16u * g);
+            const bool ok = valid(lane, 4 * g, m);
+            const float nan = __int_as_float(0x7fffffff);
+            v[4 * g] = ok ? q.x : nan;
+            v[4 * g + 1] = ok ? q.y : nan;
+            v[4 * g + 2] = ok ? q.z : nan;
+            v[4 * g + 3] = ok ? q.w : nan;
+        }
+    }
+
     __device__ __forceinline__ void lane_min_max(int m, int lane, float& mn, float& mx) const {
         mn = __int_as_float(0x7f800000);
         mx = __int_as_float(0xff800000);
@@ -591,11 +634,19 @@ __device__ __forceinline__ void early_loop(const Row& row, int kb, int max_iter,
     }
 }
 
-template <int MODE, bool TRACES, class Row>
-__device__ __forceinline__ void process_row(const Row& row, const RowOut& o, const Args& a, int lane, unsigned sbase) {
+struct NoHook {
+    __device__ __forceinline__ void operator()() const {}
+};
+
+// `after_load` runs once the row's registers have been consumed by min/max
+// (the pipelined kernel refills the row's shared-memory slot there).
+template <int MODE, bool TRACES, class Row, class Hook = NoHook>
+__device__ __forceinline__ void process_row(const Row& row, const RowOut& o, const Args& a, int lane, unsigned sbase,
+                                            const Hook& after_load = Hook()) {
     const long long r = o.r;
     float mnl, mxl;
     row.lane_min_max(a.m, lane, mnl, mxl);
+    after_load();
     const float mn0 = warp_min_nan(mnl), mx0 = warp_max(mxl);
     if (mn0 != mn0) {  // batch.py:37-39: the row holds a NaN
         if (lane == 0 && a.nan_row) atomicMin(a.nan_row, (unsigned)r);
@@ -686,7 +737,7 @@ __device__ __forceinline__ void process_row(const Row& row, const RowOut& o, con
 // predicated register copies sit behind the load).  Dynamic shared memory:
 // one staging buffer of (value, index) pairs per warp (staged rows only).
 template <int MODE, class Row, bool TRACES>
-__global__ void __launch_bounds__(256, RTK_MIN_CTAS) rowtopk_kernel(Args a) {
+__global__ void __launch_bounds__(RTK_CTA_THREADS, RTK_MIN_CTAS) rowtopk_kernel(Args a) {
     extern __shared__ __align__(16) float smem[];
     const int lane = threadIdx.x & 31;
     const unsigned per_warp = Row::kPad ? (unsigned)Row::kPad : (unsigned)a.k;  // staging entries
@@ -717,6 +768,56 @@ __global__ void __launch_bounds__(256, RTK_MIN_CTAS) rowtopk_kernel(Args a) {
         if (!more2) break;
         o.r += nw; o.ov += ostep; o.oi += ostep; o.it += nw; o.rs += nw;
     }
+}
+
+// Pipelined variant for the lane-contiguous tiles: each warp keeps a ring of
+// DEPTH row slots in shared memory filled by cp.async (LDGSTS) DEPTH grid
+// steps ahead, so DEPTH rows per warp are in flight instead of one register
+// tile.  Dynamic shared memory per warp: the selection staging buffer
+// (kPad pairs) followed by the DEPTH-slot row ring.
+#ifndef RTK_PIPE_DEPTH
+#define RTK_PIPE_DEPTH 3
+#endif
+template <int MODE, class Row, bool TRACES>
+__global__ void __launch_bounds__(RTK_CTA_THREADS, RTK_MIN_CTAS) rowtopk_pipe_kernel(Args a) {
+    constexpr int D = RTK_PIPE_DEPTH;
+    extern __shared__ __align__(16) float smem[];
+    const int lane = threadIdx.x & 31;
+    const int wid = __shfl_sync(kFull, (int)(threadIdx.x >> 5), 0);
+    const unsigned nwarps_cta = blockDim.x >> 5;
+    const unsigned base = (unsigned)__cvta_generic_to_shared(smem);
+    const unsigned sbase = base + (unsigned)wid * 8u * (unsigned)Row::kPad;
+    const unsigned ring = base + nwarps_cta * 8u * (unsigned)Row::kPad + (unsigned)wid * D * Row::kRowBytes;
+    const long long nw = (long long)gridDim.x * nwarps_cta;
+    long long r = (long long)blockIdx.x * nwarps_cta + wid;
+    if (r >= a.n) return;
+    const long long xstep = nw * a.ldx, ostep = nw * a.ldo;
+    const float* xp = a.x + r * a.ldx;
+    // prologue: rows r, r+nw, ..., r+(D-1)nw
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+        if (r + d * nw < a.n) Row::stage_async(xp + d * xstep, a.m, lane, ring + d * Row::kRowBytes);
+        cp_async_commit();
+    }
+    RowOut o{a.vals + r * a.ldo, a.idx + r * a.ldo, a.iters + r, a.reasons + r, r};
+    const float* xpre = xp + D * xstep;  // row refilled into the slot just read
+    unsigned slot = 0;
+    Row row;
+    for (;;) {
+        cp_async_wait<D - 1>();  // this row's group has landed
+        row.load_smem(ring + slot * Row::kRowBytes, a.m, lane);
+        const bool refill = o.r + D * nw < a.n;
+        const unsigned sl = ring + slot * Row::kRowBytes;
+        process_row<MODE, TRACES>(row, o, a, lane, sbase, [&] {
+            if (refill) Row::stage_async(xpre, a.m, lane, sl);
+            cp_async_commit();
+        });
+        if (o.r + nw >= a.n) break;
+        o.r += nw; o.ov += ostep; o.oi += ostep; o.it += nw; o.rs += nw;
+        xpre += xstep;
+        slot = slot + 1 == D ? 0 : slot + 1;
+    }
+    cp_async_wait<0>();
 }
 
 // k == M shortcut (_kernels.py:173-179): copy the row, indices 0..M-1, trace (0, DEGENERATE).
