@@ -121,10 +121,13 @@ int launch_pipe_kernel(const rtk::Args& a, cudaStream_t s) {
 
 template <int MODE, int E>
 int launch_lane(const rtk::Args& a, cudaStream_t s) {
-#ifndef RTK_NO_PIPE
-    if (a.m == 32 * E) return launch_pipe_kernel<MODE, rtk::LaneRow<E, false, false>>(a, s);
-    return launch_pipe_kernel<MODE, rtk::LaneRow<E, true, false>>(a, s);
-#endif
+    // The cp.async row ring pays off where registers, not shared memory, limit
+    // occupancy (measured: +5% at M = 512; -48% at M = 1024, where the ring
+    // plus the staging buffer leave one CTA per SM).
+    if constexpr (E == 16) {
+        if (a.m == 32 * E) return launch_pipe_kernel<MODE, rtk::LaneRow<E, false, false>>(a, s);
+        return launch_pipe_kernel<MODE, rtk::LaneRow<E, true, false>>(a, s);
+    }
     // staging buffer: 32*E (value, index) pairs per warp (no selection in trace mode)
     const size_t smem = MODE == rtk::kTrace ? 0 : (size_t)(kThreads / 32) * 32 * E * 8;
     const bool wide = (reinterpret_cast<uintptr_t>(a.x) & 31) == 0 && a.ldx % 8 == 0;  // 256-bit loads

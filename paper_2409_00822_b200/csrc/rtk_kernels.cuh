@@ -38,7 +38,7 @@ enum Mode : int { kExact = 0, kEarly = 1, kTrace = 2 };
 #define RTK_MIN_CTAS 1  // __launch_bounds__ min CTAs per SM for the row kernels
 #endif
 #ifndef RTK_CTA_THREADS
-#define RTK_CTA_THREADS 256  // threads per CTA of the row kernels
+#define RTK_CTA_THREADS 512  // threads per CTA of the row kernels (measured best at M = 256)
 #endif
 
 struct Args {
