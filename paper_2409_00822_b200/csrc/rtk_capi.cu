@@ -140,6 +140,10 @@ template <int MODE>
 int dispatch(const rtk::Args& a, cudaStream_t s) {
     const int m = a.m;
     const bool vec4 = (m % 4 == 0) && (a.ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
+#ifdef RTK_TUNE_E8  // tuning builds: only the M = 256 register tile (fast to compile)
+    if (m == 256 && vec4) return launch_lane<MODE, 8>(a, s);
+    return launch_row_kernel<MODE, rtk::GlobalRow>(a, s, 0);
+#else
     if (m <= 1024 && vec4) {
         // elements per lane: ceil(m / 32) rounded up to a multiple of 4
         switch ((m + 127) / 128) {
@@ -163,6 +167,7 @@ int dispatch(const rtk::Args& a, cudaStream_t s) {
         return launch_reg<MODE, 1, 32>(a, s);
     }
     return launch_row_kernel<MODE, rtk::GlobalRow>(a, s, 0);
+#endif
 }
 
 int launch_flat(void (*kernel)(rtk::Args), const rtk::Args& a, cudaStream_t s) {
@@ -182,6 +187,7 @@ int check_common(const float* x, int64_t n, int64_t m, int64_t ldx) {
     if (m < 1 || m > 0x7fffffff) return fail(RTK_EINVAL, "m must be in [1, 2^31), got %lld", (long long)m);
     if (n >= 0xffffffffLL) return fail(RTK_EINVAL, "n must be < 2^32 - 1, got %lld", (long long)n);
     if (ldx < m) return fail(RTK_EINVAL, "ldx (%lld) < m (%lld)", (long long)ldx, (long long)m);
+    if (ldx >= (1LL << 30)) return fail(RTK_EINVAL, "ldx must be < 2^30, got %lld", (long long)ldx);
     if (n > 0 && !x) return fail(RTK_EINVAL, "x is NULL");
     return RTK_OK;
 }
@@ -210,6 +216,7 @@ rtk::Args make_args(const float* x, int64_t n, int64_t m, int64_t ldx, int32_t k
     a.iters = iters;
     a.reasons = reinterpret_cast<signed char*>(reasons);
     a.nan_row = nan_first_row;
+    a.opaque_zero = 0;
     return a;
 }
 
@@ -221,6 +228,7 @@ int rowtopk_common(int mode, const float* x, int64_t n, int64_t m, int64_t ldx, 
     if (k < 1 || k > m) return fail(RTK_EINVAL, "k must be in [1, %lld], got %d", (long long)m, k);
     if (mode != rtk::kTrace) {
         if (ldo < k) return fail(RTK_EINVAL, "ldo (%lld) < k (%d)", (long long)ldo, k);
+        if (ldo >= (1LL << 30)) return fail(RTK_EINVAL, "ldo must be < 2^30, got %lld", (long long)ldo);
         if (n > 0 && (!vals || !idx)) return fail(RTK_EINVAL, "vals/idx is NULL");
     } else if (n > 0 && (!iters || !reasons)) {
         return fail(RTK_EINVAL, "iters/reasons are required for the trace kernel");

@@ -56,6 +56,9 @@ struct Args {
     int* __restrict__ iters;
     signed char* __restrict__ reasons;
     unsigned* __restrict__ nan_row;
+    // Always 0 at run time; ANDed into the next row's load offset so that the
+    // load depends on the current row's lane min/max (see rowtopk_kernel).
+    unsigned opaque_zero;
 };
 
 // ---------------------------------------------------------------- scalars
@@ -561,16 +564,6 @@ struct GlobalRow {
 // each body (before the next body's hard-cap test, the reference order).
 // SAFE: |mn0|,|mx0| < 2^126 so the midpoint cannot overflow.
 // cnt is returned biased by kCountBias.
-// Per-row output cursor: advanced by a fixed stride per grid step instead of
-// recomputing 64-bit row offsets.
-struct RowOut {
-    float* __restrict__ ov;
-    int* __restrict__ oi;
-    int* __restrict__ it;
-    signed char* __restrict__ rs;
-    long long r;
-};
-
 template <bool FP, bool SAFE, class Row>
 __device__ __forceinline__ int exact_loop(const Row& row, int kb, double eps, int cap, float& mn, float& mx,
                                           float& thres, int& cnt, int& it, int& lane_last) {
@@ -620,6 +613,51 @@ __device__ __forceinline__ int exact_loop(const Row& row, int kb, double eps, in
     }
 }
 
+// Fast form of the FP && SAFE loop for launches without traces: up to
+// `steps` reference bisection steps with no no-progress tests, leaving the
+// loop on cnt == k.  Why it is exact:
+//   * mid = RN((mn+mx)/2) is strictly inside (mn, mx) whenever a float lies
+//     strictly between them; otherwise it equals an endpoint ("stuck"), the
+//     update below is then a no-op, and every later step repeats it.
+//   * Before the first step with cnt == k, the bracket keeps
+//     mn <= x_{k+1} < x_k <= mx (x_j = j-th largest); x_k is a float strictly
+//     above mn, so a stuck step before the first cnt == k step means no
+//     later step can ever reach cnt == k.  Hence when this loop leaves on
+//     cnt == k, no reference exit fired earlier and the state equals the
+//     reference's (COUNT_EQUALS_K at the same step).
+//   * Otherwise the state after `steps` steps is the reference state (frozen
+//     since the stuck step, if any); the caller resumes with exact_loop, whose
+//     first step then reproduces the reference's INTERVAL_BELOW_EPSILON exit
+//     (same mid, same count), or continues the search.  Only the reported
+//     iteration of such a stuck exit would differ, and this form is not used
+//     when traces are requested.
+// Returns true on cnt == k; cnt biased by kCountBias.
+template <class Row>
+__device__ __forceinline__ bool exact_loop_fast(const Row& row, int kb, int steps, float& mn, float& mx, float& thres,
+                                                int& cnt, int& it, int& lane_last) {
+    float mid;
+    int c, lc;
+#pragma unroll 1
+    for (;;) {
+        ++it;
+        mid = mid_fast(mn, mx);
+        lc = row.lane_count_ge(mid);
+        c = warp_count(lc);
+        const bool lt = c < kb;
+        mx = lt ? mid : mx;
+        mn = lt ? mn : mid;
+        if (c == kb || it >= steps) break;
+    }
+    thres = mid;
+    cnt = c;
+    lane_last = lc;
+    return c == kb;
+}
+
+#ifndef RTK_FAST_STEPS
+#define RTK_FAST_STEPS 24  // fast steps before the general loop takes over (stuck rows)
+#endif
+
 // Algorithm 2 loop (_kernels.py:96-102): exactly max_iter steps; also tracks
 // this lane's count at the final lower bound (the selection threshold).
 template <bool SAFE, class Row>
@@ -635,26 +673,38 @@ __device__ __forceinline__ void early_loop(const Row& row, int kb, int max_iter,
 }
 
 struct NoHook {
-    __device__ __forceinline__ void operator()() const {}
+    __device__ __forceinline__ void operator()(unsigned) const {}
 };
 
-// `after_load` runs once the row's registers have been consumed by min/max
-// (the pipelined kernel refills the row's shared-memory slot there).
+// Byte offset of row r in a matrix with row stride `ld_bytes` (< 2^32).
+template <class T>
+__device__ __forceinline__ T* row_ptr(T* base, unsigned r, unsigned ld_bytes) {
+    return reinterpret_cast<T*>(reinterpret_cast<char*>(base) + (unsigned long long)r * ld_bytes);
+}
+template <class T>
+__device__ __forceinline__ const T* row_ptr(const T* base, unsigned r, unsigned ld_bytes) {
+    return reinterpret_cast<const T*>(reinterpret_cast<const char*>(base) + (unsigned long long)r * ld_bytes);
+}
+
+// `after_load(token)` runs once the row's registers have been consumed by
+// the lane-local min/max; `token` is derived from that min/max, so a load
+// issued there with `token & opaque_zero` in its address cannot be hoisted
+// above the consumption of this row (the next row's prefetch goes there).
 template <int MODE, bool TRACES, class Row, class Hook = NoHook>
-__device__ __forceinline__ void process_row(const Row& row, const RowOut& o, const Args& a, int lane, unsigned sbase,
+__device__ __forceinline__ void process_row(const Row& row, unsigned r, const Args& a, int lane, unsigned sbase,
                                             const Hook& after_load = Hook()) {
-    const long long r = o.r;
     float mnl, mxl;
     row.lane_min_max(a.m, lane, mnl, mxl);
-    after_load();
+    after_load(__float_as_uint(mnl) ^ __float_as_uint(mxl));
     const float mn0 = warp_min_nan(mnl), mx0 = warp_max(mxl);
     if (mn0 != mn0) {  // batch.py:37-39: the row holds a NaN
-        if (lane == 0 && a.nan_row) atomicMin(a.nan_row, (unsigned)r);
+        if (lane == 0 && a.nan_row) atomicMin(a.nan_row, r);
     }
     const int k = a.k;
     const int kb = k + kCountBias;
-    float* ov = o.ov;
-    int* oi = o.oi;
+    const unsigned ldo_b = (unsigned)a.ldo * 4u;
+    float* ov = row_ptr(a.vals, r, ldo_b);
+    int* oi = row_ptr(a.idx, r, ldo_b);
     int it = 0, reason;
     const bool safe = fabsf(mn0) < 0x1p126f && fabsf(mx0) < 0x1p126f;
 
@@ -689,7 +739,17 @@ __device__ __forceinline__ void process_row(const Row& row, const RowOut& o, con
             if (!(isfinite(mx0) && mx0 > mn0)) {
                 reason = kExitDegenerateRow;  // eps = 0*mx0 is NaN for infinite mx0
             } else if (safe) {
-                reason = exact_loop<true, true>(row, kb, 0.0, cap, mn, mx, thres, cnt, it, lane_t);
+                if constexpr (!TRACES) {
+                    const int steps = min(cap, RTK_FAST_STEPS);
+                    if (exact_loop_fast(row, kb, steps, mn, mx, thres, cnt, it, lane_t))
+                        reason = kExitCountEqualsK;
+                    else if (it >= cap)
+                        reason = kExitHardCapReached;  // selection below treats HARD_CAP and IBE alike
+                    else
+                        reason = exact_loop<true, true>(row, kb, 0.0, cap, mn, mx, thres, cnt, it, lane_t);
+                } else {
+                    reason = exact_loop<true, true>(row, kb, 0.0, cap, mn, mx, thres, cnt, it, lane_t);
+                }
             } else {
                 reason = exact_loop<true, false>(row, kb, 0.0, cap, mn, mx, thres, cnt, it, lane_t);
             }
@@ -725,17 +785,21 @@ __device__ __forceinline__ void process_row(const Row& row, const RowOut& o, con
     }
     if constexpr (TRACES) {
         if (lane == 0) {
-            *o.it = it;
-            *o.rs = (signed char)reason;
+            a.iters[r] = it;
+            a.reasons[r] = (signed char)reason;
         }
     }
 }
 
-// Persistent grid-stride row loop; each warp prefetches its next row into a
-// second register tile while the current one is searched (the prefetch is
-// unconditional -- past the last row it re-reads the current row -- so no
-// predicated register copies sit behind the load).  Dynamic shared memory:
-// one staging buffer of (value, index) pairs per warp (staged rows only).
+// Persistent grid-stride row loop.  Each warp prefetches its next row into a
+// second register tile once the current tile has been read by the lane
+// min/max: the prefetch address carries `token & opaque_zero`, so ptxas
+// cannot issue it earlier.  (Issued earlier, the two tiles' loads share one
+// scoreboard slot and the first use of the current tile waits for the
+// just-issued prefetch too -- a full DRAM latency per row.)  Past the last
+// row the prefetch re-reads the last row.  Dynamic shared memory: one
+// staging buffer of (value, index) pairs per warp (staged rows only).
+// Row indices are 32-bit (the host checks n < 2^32 - 1, row strides < 2^30).
 template <int MODE, class Row, bool TRACES>
 __global__ void __launch_bounds__(RTK_CTA_THREADS, RTK_MIN_CTAS) rowtopk_kernel(Args a) {
     extern __shared__ __align__(16) float smem[];
@@ -746,27 +810,29 @@ __global__ void __launch_bounds__(RTK_CTA_THREADS, RTK_MIN_CTAS) rowtopk_kernel(
     // REDUX/SHFL collectives, and uniform registers for the row bookkeeping).
     const int wid = __shfl_sync(kFull, (int)(threadIdx.x >> 5), 0);
     const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem) + (unsigned)wid * 8u * per_warp;
-    const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
-    long long r = (long long)blockIdx.x * (blockDim.x >> 5) + wid;
-    if (r >= a.n) return;
-    const long long xstep = nw * a.ldx, ostep = nw * a.ldo;
-    const float* xp = a.x + r * a.ldx;
-    RowOut o{a.vals + r * a.ldo, a.idx + r * a.ldo, a.iters + r, a.reasons + r, r};
+    const unsigned wpc = blockDim.x >> 5;
+    const unsigned nw = gridDim.x * wpc;
+    const unsigned n = (unsigned)a.n;
+    unsigned r = blockIdx.x * wpc + (unsigned)wid;
+    if (r >= n) return;
+    const unsigned lim = n > nw ? n - nw : 0u;  // rows below lim have a successor
+    const unsigned ldx_b = (unsigned)a.ldx * 4u;
+    const unsigned oz = a.opaque_zero;
     Row A, B;
-    A.load(xp, a.m, lane);
+    A.load(row_ptr(a.x, r, ldx_b), a.m, lane);
     for (;;) {
-        const bool more1 = o.r + nw < a.n;
-        xp += more1 ? xstep : 0;
-        B.load(xp, a.m, lane);
-        process_row<MODE, TRACES>(A, o, a, lane, sbase);
+        const bool more1 = r < lim;
+        const unsigned r1 = more1 ? r + nw : r;
+        process_row<MODE, TRACES>(A, r, a, lane, sbase,
+                                  [&](unsigned tok) { B.load(row_ptr(a.x, r1, ldx_b) + (tok & oz), a.m, lane); });
         if (!more1) break;
-        o.r += nw; o.ov += ostep; o.oi += ostep; o.it += nw; o.rs += nw;
-        const bool more2 = o.r + nw < a.n;
-        xp += more2 ? xstep : 0;
-        A.load(xp, a.m, lane);
-        process_row<MODE, TRACES>(B, o, a, lane, sbase);
+        r = r1;
+        const bool more2 = r < lim;
+        const unsigned r2 = more2 ? r + nw : r;
+        process_row<MODE, TRACES>(B, r, a, lane, sbase,
+                                  [&](unsigned tok) { A.load(row_ptr(a.x, r2, ldx_b) + (tok & oz), a.m, lane); });
         if (!more2) break;
-        o.r += nw; o.ov += ostep; o.oi += ostep; o.it += nw; o.rs += nw;
+        r = r2;
     }
 }
 
@@ -788,33 +854,32 @@ __global__ void __launch_bounds__(RTK_CTA_THREADS, RTK_MIN_CTAS) rowtopk_pipe_ke
     const unsigned base = (unsigned)__cvta_generic_to_shared(smem);
     const unsigned sbase = base + (unsigned)wid * 8u * (unsigned)Row::kPad;
     const unsigned ring = base + nwarps_cta * 8u * (unsigned)Row::kPad + (unsigned)wid * D * Row::kRowBytes;
-    const long long nw = (long long)gridDim.x * nwarps_cta;
-    long long r = (long long)blockIdx.x * nwarps_cta + wid;
-    if (r >= a.n) return;
-    const long long xstep = nw * a.ldx, ostep = nw * a.ldo;
-    const float* xp = a.x + r * a.ldx;
+    const unsigned nw = gridDim.x * nwarps_cta;
+    const unsigned n = (unsigned)a.n;
+    unsigned r = blockIdx.x * nwarps_cta + (unsigned)wid;
+    if (r >= n) return;
+    const unsigned ldx_b = (unsigned)a.ldx * 4u;
     // prologue: rows r, r+nw, ..., r+(D-1)nw
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-        if (r + d * nw < a.n) Row::stage_async(xp + d * xstep, a.m, lane, ring + d * Row::kRowBytes);
+        const unsigned long long rd = (unsigned long long)r + (unsigned long long)d * nw;
+        if (rd < n) Row::stage_async(row_ptr(a.x, (unsigned)rd, ldx_b), a.m, lane, ring + d * Row::kRowBytes);
         cp_async_commit();
     }
-    RowOut o{a.vals + r * a.ldo, a.idx + r * a.ldo, a.iters + r, a.reasons + r, r};
-    const float* xpre = xp + D * xstep;  // row refilled into the slot just read
     unsigned slot = 0;
     Row row;
     for (;;) {
         cp_async_wait<D - 1>();  // this row's group has landed
         row.load_smem(ring + slot * Row::kRowBytes, a.m, lane);
-        const bool refill = o.r + D * nw < a.n;
+        const unsigned long long rpre = (unsigned long long)r + (unsigned long long)D * nw;
+        const bool refill = rpre < n;
         const unsigned sl = ring + slot * Row::kRowBytes;
-        process_row<MODE, TRACES>(row, o, a, lane, sbase, [&] {
-            if (refill) Row::stage_async(xpre, a.m, lane, sl);
+        process_row<MODE, TRACES>(row, r, a, lane, sbase, [&](unsigned) {
+            if (refill) Row::stage_async(row_ptr(a.x, (unsigned)rpre, ldx_b), a.m, lane, sl);
             cp_async_commit();
         });
-        if (o.r + nw >= a.n) break;
-        o.r += nw; o.ov += ostep; o.oi += ostep; o.it += nw; o.rs += nw;
-        xpre += xstep;
+        if ((unsigned long long)r + nw >= n) break;
+        r += nw;
         slot = slot + 1 == D ? 0 : slot + 1;
     }
     cp_async_wait<0>();
