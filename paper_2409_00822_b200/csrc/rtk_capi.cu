@@ -14,6 +14,7 @@
 
 #include "rtk.h"
 #include "rtk_kernels.cuh"
+#include "rtk_pair.cuh"
 
 namespace {
 
@@ -27,6 +28,9 @@ int fail(int code, const char* fmt, ...) {
     return code;
 }
 
+#ifndef RTK_PAIR_MAX_E
+#define RTK_PAIR_MAX_E 8  // largest elements-per-lane tile routed to the paired-row kernel
+#endif
 constexpr int kThreads = RTK_CTA_THREADS;  // threads per CTA of the row kernels
 constexpr int kFlatThreads = 256;         // threads per CTA of the elementwise kernels
 constexpr int kMaxDevices = 64;
@@ -119,8 +123,35 @@ int launch_pipe_kernel(const rtk::Args& a, cudaStream_t s) {
     }
 }
 
+// Paired-row kernel (rtk_pair.cuh): launches without traces; exact mode
+// only with eps_rel == 0.
+template <int MODE, int E>
+bool pair_eligible(const rtk::Args& a) {
+    if constexpr (MODE == rtk::kTrace || E > RTK_PAIR_MAX_E) {
+        return false;
+    } else {
+        if (a.iters != nullptr || a.reasons != nullptr) return false;
+        return MODE == rtk::kEarly || a.eps_rel == 0.0;
+    }
+}
+
+template <int MODE, int E>
+int launch_pair(const rtk::Args& a, cudaStream_t s) {
+    if constexpr (MODE == rtk::kTrace || E > RTK_PAIR_MAX_E) {
+        return fail(RTK_EINVAL, "internal: paired-row kernel not instantiated");
+    } else {
+        // two selection staging buffers (32*E pairs each) per warp
+        const size_t smem = (size_t)(kThreads / 32) * 2 * 32 * E * 8;
+        const bool wide = (reinterpret_cast<uintptr_t>(a.x) & 31) == 0 && a.ldx % 8 == 0;  // 256-bit loads
+        if (a.m == 32 * E && wide) return launch_rows(rtk::rowtopk_pair_kernel<MODE, E, false, true>, a, s, smem);
+        if (a.m == 32 * E) return launch_rows(rtk::rowtopk_pair_kernel<MODE, E, false, false>, a, s, smem);
+        return launch_rows(rtk::rowtopk_pair_kernel<MODE, E, true, false>, a, s, smem);
+    }
+}
+
 template <int MODE, int E>
 int launch_lane(const rtk::Args& a, cudaStream_t s) {
+    if (pair_eligible<MODE, E>(a)) return launch_pair<MODE, E>(a, s);
     // The cp.async row ring pays off where registers, not shared memory, limit
     // occupancy (measured: +5% at M = 512; -48% at M = 1024, where the ring
     // plus the staging buffer leave one CTA per SM).

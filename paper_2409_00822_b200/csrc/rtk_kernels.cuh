@@ -431,21 +431,52 @@ struct LaneRow {
         return MASKED ? max(0, min(E, m - lane * E)) : E;
     }
 
-    // Stage every element with v >= t at its output position (the caller
-    // guarantees #{v >= t} >= k and flushes only the first k entries; the
-    // staging buffer holds kPad entries, so no per-element cutoff is needed).
-    // lane_hits: #{v >= t} in this lane, already known from the search pass
-    // at t (the lane input of that pass's REDUX).
-    __device__ __forceinline__ void select_ge(float t, int, unsigned sbase, int lane, int lane_hits) const {
-        const unsigned cl = (unsigned)lane_hits;
-        const unsigned excl = warp_incl_scan(cl) - cl;
-        unsigned addr = sbase + 8u * excl;
+    // Selection staging (per warp, kPad * 8 bytes of shared memory): the
+    // first half holds a copy of the row (lane l's E values at l*E), the
+    // second half the selected indices in output order.  Only indices are
+    // staged per element (one predicated STS.32 each, no register pairing);
+    // flush() looks the values up in the row copy.
+    static constexpr unsigned kIdxOff = 4u * 32u * E;
+
+    __device__ __forceinline__ void stage_row(unsigned sbase, int lane) const {
+        const unsigned dst = sbase + (unsigned)lane * E * 4u;
+#pragma unroll
+        for (int g = 0; g < E / 4; ++g)
+            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst + 16u * g), "f"(v[4 * g]),
+                         "f"(v[4 * g + 1]), "f"(v[4 * g + 2]), "f"(v[4 * g + 3])
+                         : "memory");
+    }
+
+    // Stage this lane's elements with v >= t at output positions excl,
+    // excl + 1, ... (excl: exclusive prefix of the lane hit counts).
+    __device__ __forceinline__ void stage_idx(float t, unsigned sbase, int lane, unsigned excl) const {
+        unsigned addr = sbase + kIdxOff + 4u * excl;
         const int i0 = lane * E;
 #pragma unroll
         for (int q = 0; q < E; ++q) {
             if (v[q] >= t) {
-                stage_put(addr, v[q], i0 + q);
-                addr += 8u;
+                asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(i0 + q) : "memory");
+                addr += 4u;
+            }
+        }
+    }
+
+    // Stage every element with v >= t at its output position (the caller
+    // guarantees #{v >= t} >= k and flushes only the first k entries; the
+    // staging buffer holds 32*E entries, so no per-element cutoff is needed).
+    // lane_hits: #{v >= t} in this lane, already known from the search pass
+    // at t (the lane input of that pass's REDUX).
+    __device__ __forceinline__ void select_ge(float t, int, unsigned sbase, int lane, int lane_hits) const {
+        stage_row(sbase, lane);
+        const unsigned cl = (unsigned)lane_hits;
+        const unsigned excl = warp_incl_scan(cl) - cl;
+        unsigned addr = sbase + kIdxOff + 4u * excl;
+        const int i0 = lane * E;
+#pragma unroll
+        for (int q = 0; q < E; ++q) {
+            if (v[q] >= t) {
+                asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(i0 + q) : "memory");
+                addr += 4u;
             }
         }
     }
@@ -453,6 +484,7 @@ struct LaneRow {
     // All v >= t plus the first `need` elements of [lo, t), ascending index
     // (_kernels.py:126-145).  Cold on benchmark data.
     __device__ __forceinline__ void select_fill(float t, float lo, int need, int, unsigned sbase, int lane) const {
+        stage_row(sbase, lane);
         bool pa[E], pb[E];
         unsigned packed = 0;
 #pragma unroll
@@ -464,16 +496,33 @@ struct LaneRow {
         const unsigned excl = warp_incl_scan(packed) - packed;
         int ea = (int)(excl & 0xffffu), eb = (int)(excl >> 16);
         const int i0 = lane * E;
+        const unsigned ib = sbase + kIdxOff;
 #pragma unroll
         for (int q = 0; q < E; ++q) {
             if (pa[q]) {
-                stage_put(sbase + 8u * (ea + min(eb, need)), v[q], i0 + q);
+                asm volatile("st.shared.b32 [%0], %1;" ::"r"(ib + 4u * (ea + min(eb, need))), "r"(i0 + q) : "memory");
                 ++ea;
             } else if (pb[q]) {
-                if (eb < need) stage_put(sbase + 8u * (ea + eb), v[q], i0 + q);
+                if (eb < need) asm volatile("st.shared.b32 [%0], %1;" ::"r"(ib + 4u * (ea + eb)), "r"(i0 + q) : "memory");
                 ++eb;
             }
         }
+    }
+
+    // Write the first k staged (value, index) pairs with coalesced stores.
+    __device__ __forceinline__ static void flush(unsigned sbase, int k, float* __restrict__ ov, int* __restrict__ oi,
+                                                 int lane) {
+        __syncwarp();
+#pragma unroll 1
+        for (int j = lane; j < k; j += 32) {
+            int i;
+            float x;
+            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(i) : "r"(sbase + kIdxOff + 4u * j) : "memory");
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(sbase + 4u * i) : "memory");
+            ov[j] = x;
+            oi[j] = i;
+        }
+        __syncwarp();
     }
 };
 
@@ -672,6 +721,17 @@ __device__ __forceinline__ void early_loop(const Row& row, int kb, int max_iter,
     }
 }
 
+// Staged rows: LaneRow stages indices + a row copy (LaneRow::flush), RegRow
+// stages (value, index) pairs (flush_row).
+template <class Row>
+__device__ __forceinline__ void flush_staged(unsigned sbase, int k, float* __restrict__ ov, int* __restrict__ oi,
+                                             int lane) {
+    if constexpr (Row::kPad > 0)
+        Row::flush(sbase, k, ov, oi, lane);
+    else
+        flush_row(sbase, k, ov, oi, lane);
+}
+
 struct NoHook {
     __device__ __forceinline__ void operator()(unsigned) const {}
 };
@@ -686,20 +746,46 @@ __device__ __forceinline__ const T* row_ptr(const T* base, unsigned r, unsigned 
     return reinterpret_cast<const T*>(reinterpret_cast<const char*>(base) + (unsigned long long)r * ld_bytes);
 }
 
-// `after_load(token)` runs once the row's registers have been consumed by
-// the lane-local min/max; `token` is derived from that min/max, so a load
-// issued there with `token & opaque_zero` in its address cannot be hoisted
-// above the consumption of this row (the next row's prefetch goes there).
-template <int MODE, bool TRACES, class Row, class Hook = NoHook>
-__device__ __forceinline__ void process_row(const Row& row, unsigned r, const Args& a, int lane, unsigned sbase,
-                                            const Hook& after_load = Hook()) {
-    float mnl, mxl;
-    row.lane_min_max(a.m, lane, mnl, mxl);
-    after_load(__float_as_uint(mnl) ^ __float_as_uint(mxl));
-    const float mn0 = warp_min_nan(mnl), mx0 = warp_max(mxl);
-    if (mn0 != mn0) {  // batch.py:37-39: the row holds a NaN
-        if (lane == 0 && a.nan_row) atomicMin(a.nan_row, r);
+// select_exact (_kernels.py:149-162): threshold t = mx when the search
+// ended with cnt > k (eps_rel == 0, not degenerate), else thres; then
+// select_threshold (_kernels.py:106-146) with lo = mn.  cnt is biased.
+template <class Row>
+__device__ __forceinline__ void select_exact(const Row& row, const Args& a, int lane, unsigned sbase, bool fp,
+                                             int reason, float thres, float mn, float mx, int cnt, int lane_t,
+                                             float* __restrict__ ov, int* __restrict__ oi) {
+    const int k = a.k;
+    const bool use_mx = (cnt > k + kCountBias) && fp && (reason != kExitDegenerateRow);
+    float t = thres;
+    int ca = cnt - kCountBias;
+    if (use_mx) {
+        t = mx;
+        lane_t = row.lane_count_ge(mx);
+        ca = warp_count(lane_t) - kCountBias;
     }
+    if constexpr (Row::kStaged) {
+        if (ca >= k)
+            row.select_ge(t, k, sbase, lane, lane_t - (int)kLaneBias);
+        else
+            row.select_fill(t, mn, k - ca, k, sbase, lane);
+        flush_staged<Row>(sbase, k, ov, oi, lane);
+    } else {
+        if (ca >= k)
+            row.select_ge(t, k, ov, oi, lane, 0);
+        else
+            row.select_fill(t, mn, k - ca, k, ov, oi, lane);
+    }
+}
+
+// Rows holding a NaN: record the first offending row (batch.py:37-39).  Cold.
+__device__ __noinline__ void report_nan(unsigned* nan_row, unsigned r, int lane) {
+    if (lane == 0 && nan_row) atomicMin(nan_row, r);
+}
+
+// Everything after the row's min/max (mn0, mx0): search, selection, flush,
+// traces -- the general per-row path (all modes, every exit rule).
+template <int MODE, bool TRACES, class Row>
+__device__ __forceinline__ void row_body(const Row& row, unsigned r, const Args& a, int lane, unsigned sbase, bool fp,
+                                         float mn0, float mx0) {
     const int k = a.k;
     const int kb = k + kCountBias;
     const unsigned ldo_b = (unsigned)a.ldo * 4u;
@@ -724,13 +810,13 @@ __device__ __forceinline__ void process_row(const Row& row, unsigned r, const Ar
         }
         if constexpr (Row::kStaged) {
             row.select_ge(mn, k, sbase, lane, lane_mn - (int)kLaneBias);
-            flush_row(sbase, k, ov, oi, lane);
+            flush_staged<Row>(sbase, k, ov, oi, lane);
         } else {
             row.select_ge(mn, k, ov, oi, lane, 0);
         }
     } else {
-        // Algorithm 1 (_kernels.py:48-84) + select_exact (_kernels.py:149-162)
-        const bool fp = (a.eps_rel == 0.0);
+        // Algorithm 1 (_kernels.py:48-84) + select_exact (_kernels.py:149-162);
+        // fp: eps_rel == 0 (hoisted by the caller).
         float mn = mn0, mx = mx0, thres = mn0;
         int cnt = a.m + kCountBias;
         int lane_t = (int)kLaneBias + Row::lane_valid(a.m, lane);  // lane count at thres
@@ -760,28 +846,7 @@ __device__ __forceinline__ void process_row(const Row& row, unsigned r, const Ar
             else
                 reason = exact_loop<false, false>(row, kb, eps, cap, mn, mx, thres, cnt, it, lane_t);
         }
-        if constexpr (MODE == kExact) {
-            const bool use_mx = (cnt > kb) && fp && (reason != kExitDegenerateRow);
-            float t = thres;
-            int ca = cnt - kCountBias;
-            if (use_mx) {
-                t = mx;
-                lane_t = row.lane_count_ge(mx);
-                ca = warp_count(lane_t) - kCountBias;
-            }
-            if constexpr (Row::kStaged) {
-                if (ca >= k)
-                    row.select_ge(t, k, sbase, lane, lane_t - (int)kLaneBias);
-                else
-                    row.select_fill(t, mn, k - ca, k, sbase, lane);
-                flush_row(sbase, k, ov, oi, lane);
-            } else {
-                if (ca >= k)
-                    row.select_ge(t, k, ov, oi, lane, 0);
-                else
-                    row.select_fill(t, mn, k - ca, k, ov, oi, lane);
-            }
-        }
+        if constexpr (MODE == kExact) select_exact(row, a, lane, sbase, fp, reason, thres, mn, mx, cnt, lane_t, ov, oi);
     }
     if constexpr (TRACES) {
         if (lane == 0) {
@@ -789,6 +854,21 @@ __device__ __forceinline__ void process_row(const Row& row, unsigned r, const Ar
             a.reasons[r] = (signed char)reason;
         }
     }
+}
+
+// `after_load(token)` runs once the row's registers have been consumed by
+// the lane-local min/max; `token` is derived from that min/max, so a load
+// issued there with `token & opaque_zero` in its address cannot be hoisted
+// above the consumption of this row (the next row's prefetch goes there).
+template <int MODE, bool TRACES, class Row, class Hook = NoHook>
+__device__ __forceinline__ void process_row(const Row& row, unsigned r, const Args& a, int lane, unsigned sbase,
+                                            bool fp, const Hook& after_load = Hook()) {
+    float mnl, mxl;
+    row.lane_min_max(a.m, lane, mnl, mxl);
+    after_load(__float_as_uint(mnl) ^ __float_as_uint(mxl));
+    const float mn0 = warp_min_nan(mnl), mx0 = warp_max(mxl);
+    if (mn0 != mn0) report_nan(a.nan_row, r, lane);
+    row_body<MODE, TRACES>(row, r, a, lane, sbase, fp, mn0, mx0);
 }
 
 // Persistent grid-stride row loop.  Each warp prefetches its next row into a
@@ -818,19 +898,20 @@ __global__ void __launch_bounds__(RTK_CTA_THREADS, RTK_MIN_CTAS) rowtopk_kernel(
     const unsigned lim = n > nw ? n - nw : 0u;  // rows below lim have a successor
     const unsigned ldx_b = (unsigned)a.ldx * 4u;
     const unsigned oz = a.opaque_zero;
+    const bool fp = a.eps_rel == 0.0;
     Row A, B;
     A.load(row_ptr(a.x, r, ldx_b), a.m, lane);
     for (;;) {
         const bool more1 = r < lim;
         const unsigned r1 = more1 ? r + nw : r;
-        process_row<MODE, TRACES>(A, r, a, lane, sbase,
-                                  [&](unsigned tok) { B.load(row_ptr(a.x, r1, ldx_b) + (tok & oz), a.m, lane); });
+        process_row<MODE, TRACES>(A, r, a, lane, sbase, fp,
+                                  [&](unsigned tok) { B.load(row_ptr(a.x, r1 + (tok & oz), ldx_b), a.m, lane); });
         if (!more1) break;
         r = r1;
         const bool more2 = r < lim;
         const unsigned r2 = more2 ? r + nw : r;
-        process_row<MODE, TRACES>(B, r, a, lane, sbase,
-                                  [&](unsigned tok) { A.load(row_ptr(a.x, r2, ldx_b) + (tok & oz), a.m, lane); });
+        process_row<MODE, TRACES>(B, r, a, lane, sbase, fp,
+                                  [&](unsigned tok) { A.load(row_ptr(a.x, r2 + (tok & oz), ldx_b), a.m, lane); });
         if (!more2) break;
         r = r2;
     }
@@ -859,6 +940,7 @@ __global__ void __launch_bounds__(RTK_CTA_THREADS, RTK_MIN_CTAS) rowtopk_pipe_ke
     unsigned r = blockIdx.x * nwarps_cta + (unsigned)wid;
     if (r >= n) return;
     const unsigned ldx_b = (unsigned)a.ldx * 4u;
+    const bool fp = a.eps_rel == 0.0;
     // prologue: rows r, r+nw, ..., r+(D-1)nw
 #pragma unroll
     for (int d = 0; d < D; ++d) {
@@ -874,7 +956,7 @@ __global__ void __launch_bounds__(RTK_CTA_THREADS, RTK_MIN_CTAS) rowtopk_pipe_ke
         const unsigned long long rpre = (unsigned long long)r + (unsigned long long)D * nw;
         const bool refill = rpre < n;
         const unsigned sl = ring + slot * Row::kRowBytes;
-        process_row<MODE, TRACES>(row, r, a, lane, sbase, [&](unsigned) {
+        process_row<MODE, TRACES>(row, r, a, lane, sbase, fp, [&](unsigned) {
             if (refill) Row::stage_async(row_ptr(a.x, (unsigned)rpre, ldx_b), a.m, lane, sl);
             cp_async_commit();
         });

@@ -1,0 +1,226 @@
+// rtk_pair.cuh -- paired-row persistent kernel (the hot path).
+//
+// Each warp processes its rows two at a time (rows r and r + nw of the
+// grid-stride sequence) in lockstep: the two rows' min/max reductions,
+// bisection steps, selection scans and output flushes are independent
+// dependency chains issued back to back, so one row's REDUX / SHFL / LDS
+// latency is covered by the other row's instructions.  The selection needs
+// one warp scan for both rows (lane hit counts packed 16 + 16 bits).  In
+// exact mode the pair loop runs until either row meets cnt == k; the other
+// row finishes its search alone (exact_loop_fast), so no step is spent on a
+// finished row.  The next pair is prefetched into a second pair of register
+// tiles once the current pair has been read (see rowtopk_kernel).
+//
+// Used for launches without traces on the lane-contiguous register tile
+// (M <= 1024, M % 4 == 0, 16-byte aligned rows) in early-stop mode and in
+// exact mode with eps_rel == 0.  Rows that cannot take the fast loop
+// (degenerate, |min| or |max| >= 2^126, NaN) and unpaired last rows run the
+// general per-row path (row_body).  Outputs are those of rowtopk_kernel.
+#pragma once
+
+#include "rtk_kernels.cuh"
+
+namespace rtk {
+
+#ifndef RTK_PAIR_MIN_CTAS
+#define RTK_PAIR_MIN_CTAS 2  // __launch_bounds__ min CTAs per SM (caps registers at 64)
+#endif
+
+// Inclusive warp prefix sum, no volatile (the compiler may interleave it).
+__device__ __forceinline__ unsigned warp_incl_scan_nv(unsigned x) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned t = __shfl_up_sync(kFull, x, d);
+        x += lane >= d ? t : 0u;
+    }
+    return x;
+}
+
+// Both rows selected at thresholds tA, tB with biased lane hit counts hA, hB
+// (#{v >= t} per lane): stage row copies and indices, then write the first k
+// (value, index) pairs of each row.
+template <class Row>
+__device__ __forceinline__ void select_flush_pair(const Row& A, const Row& B, float tA, float tB, int hA, int hB,
+                                                  unsigned sA, unsigned sB, int lane, int k, float* __restrict__ ovA,
+                                                  int* __restrict__ oiA, float* __restrict__ ovB,
+                                                  int* __restrict__ oiB) {
+    A.stage_row(sA, lane);
+    B.stage_row(sB, lane);
+    const unsigned packed = (unsigned)(hA - (int)kLaneBias) | ((unsigned)(hB - (int)kLaneBias) << 16);
+    const unsigned excl = warp_incl_scan_nv(packed) - packed;
+    A.stage_idx(tA, sA, lane, excl & 0xffffu);
+    B.stage_idx(tB, sB, lane, excl >> 16);
+    __syncwarp();
+#pragma unroll 1
+    for (int j = lane; j < k; j += 32) {
+        int iA, iB;
+        float xA, xB;
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(iA) : "r"(sA + Row::kIdxOff + 4u * j) : "memory");
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(iB) : "r"(sB + Row::kIdxOff + 4u * j) : "memory");
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xA) : "r"(sA + 4u * iA) : "memory");
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xB) : "r"(sB + 4u * iB) : "memory");
+        ovA[j] = xA;
+        oiA[j] = iA;
+        ovB[j] = xB;
+        oiB[j] = iB;
+    }
+    __syncwarp();
+}
+
+// Exact mode, one row after its fast loop ended (eq: cnt == k at mid).
+template <class Row>
+__device__ __forceinline__ void finish_exact(const Row& row, const Args& a, int lane, unsigned sbase, bool eq,
+                                             float mn, float mx, float mid, int cnt, int it, int lc,
+                                             float* __restrict__ ov, int* __restrict__ oi) {
+    const int kb = a.k + kCountBias;
+    if (eq) {
+        row.select_ge(mid, a.k, sbase, lane, lc - (int)kLaneBias);
+        flush_staged<Row>(sbase, a.k, ov, oi, lane);
+        return;
+    }
+    float thres = mid;
+    int reason;
+    if (it >= a.hard_cap)
+        reason = kExitHardCapReached;  // selection treats HARD_CAP and IBE alike
+    else
+        reason = exact_loop<true, true>(row, kb, 0.0, a.hard_cap, mn, mx, thres, cnt, it, lc);
+    select_exact(row, a, lane, sbase, true, reason, thres, mn, mx, cnt, lc, ov, oi);
+}
+
+template <int MODE, class Row>
+__device__ __forceinline__ bool fast_eligible(float mn0, float mx0) {
+    const bool ok = MODE == kEarly ? (mx0 > mn0) : (isfinite(mx0) && mx0 > mn0);
+    return ok && fabsf(mn0) < 0x1p126f && fabsf(mx0) < 0x1p126f;
+}
+
+// One pair of rows (rA = r, rB = r + nw when hasB).  `after_load(token)`
+// issues the next pair's loads once both tiles have been read.
+template <int MODE, class Row, class Hook>
+__device__ __forceinline__ void process_pair(const Row& A, const Row& B, unsigned rA, unsigned rB, bool hasB,
+                                             const Args& a, int lane, unsigned sA, unsigned sB, int steps,
+                                             const Hook& after_load) {
+    float mnlA, mxlA, mnlB, mxlB;
+    A.lane_min_max(a.m, lane, mnlA, mxlA);
+    B.lane_min_max(a.m, lane, mnlB, mxlB);
+    after_load(__float_as_uint(mnlA) ^ __float_as_uint(mxlB));
+    const float mn0A = warp_min_nan(mnlA), mx0A = warp_max(mxlA);
+    const float mn0B = warp_min_nan(mnlB), mx0B = warp_max(mxlB);
+    if (mn0A != mn0A) report_nan(a.nan_row, rA, lane);
+    if (hasB && mn0B != mn0B) report_nan(a.nan_row, rB, lane);
+    const unsigned ldo_b = (unsigned)a.ldo * 4u;
+    float* ovA = row_ptr(a.vals, rA, ldo_b);
+    int* oiA = row_ptr(a.idx, rA, ldo_b);
+    float* ovB = row_ptr(a.vals, rB, ldo_b);
+    int* oiB = row_ptr(a.idx, rB, ldo_b);
+    const int k = a.k;
+    const int kb = k + kCountBias;
+
+    if (!(hasB && fast_eligible<MODE, Row>(mn0A, mx0A) && fast_eligible<MODE, Row>(mn0B, mx0B))) {
+        row_body<MODE, false>(A, rA, a, lane, sA, true, mn0A, mx0A);
+        if (hasB) row_body<MODE, false>(B, rB, a, lane, sB, true, mn0B, mx0B);
+        return;
+    }
+
+    float mnA = mn0A, mxA = mx0A, mnB = mn0B, mxB = mx0B;
+    if constexpr (MODE == kEarly) {
+        // Algorithm 2 (_kernels.py:96-102) on both rows; lane counts at mn
+        int hA = (int)kLaneBias + Row::lane_valid(a.m, lane), hB = hA;
+#pragma unroll 1
+        for (int i = 0; i < steps; ++i) {
+            const float midA = mid_fast(mnA, mxA), midB = mid_fast(mnB, mxB);
+            const int lA = A.lane_count_ge(midA), lB = B.lane_count_ge(midB);
+            const bool ltA = warp_count(lA) < kb, ltB = warp_count(lB) < kb;
+            mxA = ltA ? midA : mxA;
+            mnA = ltA ? mnA : midA;
+            hA = ltA ? hA : lA;
+            mxB = ltB ? midB : mxB;
+            mnB = ltB ? mnB : midB;
+            hB = ltB ? hB : lB;
+        }
+        // first k indices with v >= mn (_kernels.py:205-212)
+        select_flush_pair(A, B, mnA, mnB, hA, hB, sA, sB, lane, k, ovA, oiA, ovB, oiB);
+    } else {
+        // Algorithm 1 fast steps (exact_loop_fast) on both rows until either
+        // meets cnt == k; the other continues alone.
+        float midA, midB;
+        int cA, cB, lA, lB, it = 0;
+        bool eqA, eqB;
+#pragma unroll 1
+        do {
+            ++it;
+            midA = mid_fast(mnA, mxA);
+            midB = mid_fast(mnB, mxB);
+            lA = A.lane_count_ge(midA);
+            lB = B.lane_count_ge(midB);
+            cA = warp_count(lA);
+            cB = warp_count(lB);
+            const bool ltA = cA < kb, ltB = cB < kb;
+            mxA = ltA ? midA : mxA;
+            mnA = ltA ? mnA : midA;
+            mxB = ltB ? midB : mxB;
+            mnB = ltB ? mnB : midB;
+            eqA = cA == kb;
+            eqB = cB == kb;
+        } while (!eqA && !eqB && it < steps);
+        int itA = it, itB = it;
+        if (!eqA && itA < steps) eqA = exact_loop_fast(A, kb, steps, mnA, mxA, midA, cA, itA, lA);
+        if (!eqB && itB < steps) eqB = exact_loop_fast(B, kb, steps, mnB, mxB, midB, cB, itB, lB);
+        if (eqA && eqB) {
+            select_flush_pair(A, B, midA, midB, lA, lB, sA, sB, lane, k, ovA, oiA, ovB, oiB);
+        } else {
+            finish_exact(A, a, lane, sA, eqA, mnA, mxA, midA, cA, itA, lA, ovA, oiA);
+            finish_exact(B, a, lane, sB, eqB, mnB, mxB, midB, cB, itB, lB, ovB, oiB);
+        }
+    }
+}
+
+// Persistent loop over row pairs (r, r + nw), stepping 2 nw; register
+// double buffering of the pair (the roles of the two tile pairs alternate
+// between the two unrolled halves).
+template <int MODE, int E, bool MASKED, bool WIDE>
+__global__ void __launch_bounds__(RTK_CTA_THREADS, RTK_PAIR_MIN_CTAS) rowtopk_pair_kernel(Args a) {
+    using Row = LaneRow<E, MASKED, WIDE>;
+    extern __shared__ __align__(16) float smem[];
+    const int lane = threadIdx.x & 31;
+    const int wid = __shfl_sync(kFull, (int)(threadIdx.x >> 5), 0);
+    const unsigned wpc = blockDim.x >> 5;
+    const unsigned sA = (unsigned)__cvta_generic_to_shared(smem) + (unsigned)wid * 16u * (unsigned)Row::kPad;
+    const unsigned sB = sA + 8u * (unsigned)Row::kPad;
+    const unsigned nw = gridDim.x * wpc;
+    const unsigned long long n = (unsigned long long)a.n;
+    unsigned r = blockIdx.x * wpc + (unsigned)wid;
+    if (r >= n) return;
+    const unsigned last = (unsigned)(n - 1);
+    const unsigned ldx_b = (unsigned)a.ldx * 4u;
+    const unsigned oz = a.opaque_zero;
+    const int steps = MODE == kEarly ? a.max_iter : min(a.hard_cap, RTK_FAST_STEPS);
+    auto rowp = [&](unsigned long long rr, unsigned tok) {
+        return row_ptr(a.x, (unsigned)(rr < n ? rr : last) + tok, ldx_b);
+    };
+    Row A, B, C, D;
+    A.load(rowp(r, 0), a.m, lane);
+    B.load(rowp((unsigned long long)r + nw, 0), a.m, lane);
+    for (;;) {
+        const unsigned long long rn = (unsigned long long)r + 2ull * nw;
+        process_pair<MODE>(A, B, r, r + nw, (unsigned long long)r + nw < n, a, lane, sA, sB, steps,
+                           [&](unsigned tok) {
+                               tok &= oz;
+                               C.load(rowp(rn, tok), a.m, lane);
+                               D.load(rowp(rn + nw, tok), a.m, lane);
+                           });
+        if (rn >= n) break;
+        r = (unsigned)rn;
+        const unsigned long long rn2 = (unsigned long long)r + 2ull * nw;
+        process_pair<MODE>(C, D, r, r + nw, (unsigned long long)r + nw < n, a, lane, sA, sB, steps,
+                           [&](unsigned tok) {
+                               tok &= oz;
+                               A.load(rowp(rn2, tok), a.m, lane);
+                               B.load(rowp(rn2 + nw, tok), a.m, lane);
+                           });
+        if (rn2 >= n) break;
+        r = (unsigned)rn2;
+    }
+}
+
+}  // namespace rtk
