@@ -131,6 +131,7 @@ bool pair_eligible(const rtk::Args& a) {
         return false;
     } else {
         if (a.iters != nullptr || a.reasons != nullptr) return false;
+        if (a.n >= 0xffff0000LL) return false;  // 32-bit row cursors: n + 2 * (warps in the grid) < 2^32
         return MODE == rtk::kEarly || a.eps_rel == 0.0;
     }
 }

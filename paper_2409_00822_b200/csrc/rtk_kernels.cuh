@@ -438,6 +438,13 @@ struct LaneRow {
     // flush() looks the values up in the row copy.
     static constexpr unsigned kIdxOff = 4u * 32u * E;
 
+    // A staged index is always < 32*E for NaN-free rows (#{v >= t} >= k);
+    // NaN rows (reported as an error) may leave slots unwritten, so clamp
+    // before using an index as a shared-memory offset.
+    __device__ __forceinline__ static unsigned clamp_slot(int i) {
+        return ((32u * E) & (32u * E - 1)) == 0 ? (unsigned)i & (32u * E - 1) : min((unsigned)i, 32u * E - 1);
+    }
+
     __device__ __forceinline__ void stage_row(unsigned sbase, int lane) const {
         const unsigned dst = sbase + (unsigned)lane * E * 4u;
 #pragma unroll
@@ -518,7 +525,7 @@ struct LaneRow {
             int i;
             float x;
             asm volatile("ld.shared.b32 %0, [%1];" : "=r"(i) : "r"(sbase + kIdxOff + 4u * j) : "memory");
-            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(sbase + 4u * i) : "memory");
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(sbase + 4u * clamp_slot(i)) : "memory");
             ov[j] = x;
             oi[j] = i;
         }

@@ -26,14 +26,16 @@ namespace rtk {
 #define RTK_PAIR_MIN_CTAS 2  // __launch_bounds__ min CTAs per SM (caps registers at 64)
 #endif
 
-// Inclusive warp prefix sum, no volatile (the compiler may interleave it).
+// Inclusive warp prefix sum (SHFL.UP's in-range predicate guards the add);
+// not volatile, so the compiler may schedule other work between the steps.
 __device__ __forceinline__ unsigned warp_incl_scan_nv(unsigned x) {
-    const int lane = threadIdx.x & 31;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const unsigned t = __shfl_up_sync(kFull, x, d);
-        x += lane >= d ? t : 0u;
-    }
+    for (int d = 1; d < 32; d <<= 1)
+        asm("{.reg .pred p; .reg .b32 t;\n\t"
+            "shfl.sync.up.b32 t|p, %0, %1, 0, 0xffffffff;\n\t"
+            "@p add.u32 %0, %0, t;}"
+            : "+r"(x)
+            : "r"(d));
     return x;
 }
 
@@ -52,14 +54,30 @@ __device__ __forceinline__ void select_flush_pair(const Row& A, const Row& B, fl
     A.stage_idx(tA, sA, lane, excl & 0xffffu);
     B.stage_idx(tB, sB, lane, excl >> 16);
     __syncwarp();
+    if (k <= 32) {
+        if (lane < k) {
+            int iA, iB;
+            float xA, xB;
+            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(iA) : "r"(sA + Row::kIdxOff + 4u * lane) : "memory");
+            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(iB) : "r"(sB + Row::kIdxOff + 4u * lane) : "memory");
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xA) : "r"(sA + 4u * Row::clamp_slot(iA)) : "memory");
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xB) : "r"(sB + 4u * Row::clamp_slot(iB)) : "memory");
+            ovA[lane] = xA;
+            oiA[lane] = iA;
+            ovB[lane] = xB;
+            oiB[lane] = iB;
+        }
+        __syncwarp();
+        return;
+    }
 #pragma unroll 1
     for (int j = lane; j < k; j += 32) {
         int iA, iB;
         float xA, xB;
         asm volatile("ld.shared.b32 %0, [%1];" : "=r"(iA) : "r"(sA + Row::kIdxOff + 4u * j) : "memory");
         asm volatile("ld.shared.b32 %0, [%1];" : "=r"(iB) : "r"(sB + Row::kIdxOff + 4u * j) : "memory");
-        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xA) : "r"(sA + 4u * iA) : "memory");
-        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xB) : "r"(sB + 4u * iB) : "memory");
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xA) : "r"(sA + 4u * Row::clamp_slot(iA)) : "memory");
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xB) : "r"(sB + 4u * Row::clamp_slot(iB)) : "memory");
         ovA[j] = xA;
         oiA[j] = iA;
         ovB[j] = xB;
@@ -88,10 +106,11 @@ __device__ __forceinline__ void finish_exact(const Row& row, const Args& a, int 
     select_exact(row, a, lane, sbase, true, reason, thres, mn, mx, cnt, lc, ov, oi);
 }
 
-template <int MODE, class Row>
+// mn0 < mx0 with both inside (-2^126, 2^126): non-degenerate (both modes),
+// finite (exact mode's eps_rel == 0 loop test) and overflow-free midpoints.
+// NaN compares false.
 __device__ __forceinline__ bool fast_eligible(float mn0, float mx0) {
-    const bool ok = MODE == kEarly ? (mx0 > mn0) : (isfinite(mx0) && mx0 > mn0);
-    return ok && fabsf(mn0) < 0x1p126f && fabsf(mx0) < 0x1p126f;
+    return mx0 > mn0 && mn0 > -0x1p126f && mx0 < 0x1p126f;
 }
 
 // One pair of rows (rA = r, rB = r + nw when hasB).  `after_load(token)`
@@ -116,7 +135,7 @@ __device__ __forceinline__ void process_pair(const Row& A, const Row& B, unsigne
     const int k = a.k;
     const int kb = k + kCountBias;
 
-    if (!(hasB && fast_eligible<MODE, Row>(mn0A, mx0A) && fast_eligible<MODE, Row>(mn0B, mx0B))) {
+    if (!(hasB && fast_eligible(mn0A, mx0A) && fast_eligible(mn0B, mx0B))) {
         row_body<MODE, false>(A, rA, a, lane, sA, true, mn0A, mx0A);
         if (hasB) row_body<MODE, false>(B, rB, a, lane, sB, true, mn0B, mx0B);
         return;
@@ -188,38 +207,33 @@ __global__ void __launch_bounds__(RTK_CTA_THREADS, RTK_PAIR_MIN_CTAS) rowtopk_pa
     const unsigned sA = (unsigned)__cvta_generic_to_shared(smem) + (unsigned)wid * 16u * (unsigned)Row::kPad;
     const unsigned sB = sA + 8u * (unsigned)Row::kPad;
     const unsigned nw = gridDim.x * wpc;
-    const unsigned long long n = (unsigned long long)a.n;
+    const unsigned n = (unsigned)a.n;  // the host guarantees n + 2 nw < 2^32
     unsigned r = blockIdx.x * wpc + (unsigned)wid;
     if (r >= n) return;
-    const unsigned last = (unsigned)(n - 1);
+    const unsigned last = n - 1;
     const unsigned ldx_b = (unsigned)a.ldx * 4u;
     const unsigned oz = a.opaque_zero;
     const int steps = MODE == kEarly ? a.max_iter : min(a.hard_cap, RTK_FAST_STEPS);
-    auto rowp = [&](unsigned long long rr, unsigned tok) {
-        return row_ptr(a.x, (unsigned)(rr < n ? rr : last) + tok, ldx_b);
-    };
     Row A, B, C, D;
-    A.load(rowp(r, 0), a.m, lane);
-    B.load(rowp((unsigned long long)r + nw, 0), a.m, lane);
+    A.load(row_ptr(a.x, r, ldx_b), a.m, lane);
+    B.load(row_ptr(a.x, min(r + nw, last), ldx_b), a.m, lane);
     for (;;) {
-        const unsigned long long rn = (unsigned long long)r + 2ull * nw;
-        process_pair<MODE>(A, B, r, r + nw, (unsigned long long)r + nw < n, a, lane, sA, sB, steps,
-                           [&](unsigned tok) {
-                               tok &= oz;
-                               C.load(rowp(rn, tok), a.m, lane);
-                               D.load(rowp(rn + nw, tok), a.m, lane);
-                           });
+        const unsigned rn = r + 2 * nw;
+        process_pair<MODE>(A, B, r, r + nw, r + nw < n, a, lane, sA, sB, steps, [&](unsigned tok) {
+            tok &= oz;
+            C.load(row_ptr(a.x, min(rn, last) + tok, ldx_b), a.m, lane);
+            D.load(row_ptr(a.x, min(rn + nw, last) + tok, ldx_b), a.m, lane);
+        });
         if (rn >= n) break;
-        r = (unsigned)rn;
-        const unsigned long long rn2 = (unsigned long long)r + 2ull * nw;
-        process_pair<MODE>(C, D, r, r + nw, (unsigned long long)r + nw < n, a, lane, sA, sB, steps,
-                           [&](unsigned tok) {
-                               tok &= oz;
-                               A.load(rowp(rn2, tok), a.m, lane);
-                               B.load(rowp(rn2 + nw, tok), a.m, lane);
-                           });
+        r = rn;
+        const unsigned rn2 = r + 2 * nw;
+        process_pair<MODE>(C, D, r, r + nw, r + nw < n, a, lane, sA, sB, steps, [&](unsigned tok) {
+            tok &= oz;
+            A.load(row_ptr(a.x, min(rn2, last) + tok, ldx_b), a.m, lane);
+            B.load(row_ptr(a.x, min(rn2 + nw, last) + tok, ldx_b), a.m, lane);
+        });
         if (rn2 >= n) break;
-        r = (unsigned)rn2;
+        r = rn2;
     }
 }
 
