@@ -64,6 +64,7 @@ def parse():
     p.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--shape", default=None, help="N:M:k (overrides --workload; for profiling sweeps)")
     return p.parse_args()
 
 
@@ -293,6 +294,9 @@ def main():
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     n_cfg, m, k = WORKLOADS[args.workload]
+    if args.shape:
+        n_cfg, m, k = (int(v) for v in args.shape.split(":"))
+        args.workload = f"custom {args.shape}"
     n = n_cfg // world if args.strong else n_cfg
     if args.strong:
         from paper_2409_00822_b200.shard import shard_range

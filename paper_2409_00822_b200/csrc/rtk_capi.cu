@@ -15,6 +15,7 @@
 #include "rtk.h"
 #include "rtk_kernels.cuh"
 #include "rtk_pair.cuh"
+#include "rtk_big.cuh"
 
 namespace {
 
@@ -28,6 +29,9 @@ int fail(int code, const char* fmt, ...) {
     return code;
 }
 
+#ifndef RTK_BIG_MIN_E
+#define RTK_BIG_MIN_E 12  // smallest elements-per-lane tile routed to the long-row kernel
+#endif
 #ifndef RTK_PAIR_MAX_E
 #define RTK_PAIR_MAX_E 8  // largest elements-per-lane tile routed to the paired-row kernel
 #endif
@@ -59,29 +63,29 @@ int device_sms() {
 std::mutex g_occ_mu;
 std::map<std::tuple<int, const void*, size_t>, int> g_occ;
 
-int ctas_per_sm(const void* kernel, size_t smem) {
+int ctas_per_sm(const void* kernel, size_t smem, int threads) {
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(g_occ_mu);
-    auto key = std::make_tuple(dev, kernel, smem);
+    auto key = std::make_tuple(dev, kernel, smem + ((size_t)threads << 40));
     auto it = g_occ.find(key);
     if (it != g_occ.end()) return it->second;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int blocks = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, kThreads, smem) != cudaSuccess || blocks < 1)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, threads, smem) != cudaSuccess || blocks < 1)
         blocks = 1;
     g_occ[key] = blocks;
     return blocks;
 }
 
 template <class K>
-int launch_rows(K kernel, const rtk::Args& a, cudaStream_t s, size_t smem) {
+int launch_rows(K kernel, const rtk::Args& a, cudaStream_t s, size_t smem, int threads = kThreads) {
     const long long warps_needed = a.n;
-    const long long blocks_needed = (warps_needed + (kThreads / 32) - 1) / (kThreads / 32);
-    long long grid = (long long)device_sms() * ctas_per_sm(reinterpret_cast<const void*>(kernel), smem);
+    const long long blocks_needed = (warps_needed + (threads / 32) - 1) / (threads / 32);
+    long long grid = (long long)device_sms() * ctas_per_sm(reinterpret_cast<const void*>(kernel), smem, threads);
     if (grid > blocks_needed) grid = blocks_needed;
     if (grid < 1) grid = 1;
-    kernel<<<(unsigned)grid, kThreads, smem, s>>>(a);
+    kernel<<<(unsigned)grid, threads, smem, s>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(RTK_ECUDA, "kernel launch failed: %s", cudaGetErrorString(e));
     return RTK_OK;
@@ -104,22 +108,29 @@ int launch_row_kernel(const rtk::Args& a, cudaStream_t s, size_t smem) {
 template <int MODE, int V, int C>
 int launch_reg(const rtk::Args& a, cudaStream_t s) {
     // staging buffer: k (value, index) pairs per warp (no selection in trace mode)
-    const size_t smem = MODE == rtk::kTrace ? 0 : (size_t)(kThreads / 32) * 2 * a.k * sizeof(float);
+    const size_t smem = MODE == rtk::kTrace ? 0 : (size_t)(kThreads / 32) * rtk::RegRow<V, C, false>::stage_bytes(a.k);
     if (a.m == C * 32 * V) return launch_row_kernel<MODE, rtk::RegRow<V, C, false>>(a, s, smem);
     return launch_row_kernel<MODE, rtk::RegRow<V, C, true>>(a, s, smem);
 }
 
-template <int MODE, class Row>
-int launch_pipe_kernel(const rtk::Args& a, cudaStream_t s) {
-    // per warp: selection staging (kPad pairs) + RTK_PIPE_DEPTH row slots
-    const size_t smem = (size_t)(kThreads / 32) * (8 * Row::kPad + RTK_PIPE_DEPTH * Row::kRowBytes);
+// Long rows (rtk_big.cuh): one register tile, cp.async ring, k-pair staging.
+template <int MODE, int E, bool MASKED, bool TRACES>
+int launch_big_kernel(const rtk::Args& a, cudaStream_t s) {
+    using Row = rtk::LaneRowCut<E, MASKED>;
+    constexpr int wpc = RTK_BIG_THREADS / 32;
+    const size_t smem = (size_t)wpc * (Row::stage_bytes(a.k) + RTK_BIG_DEPTH * Row::kRowBytes);
+    return launch_rows(rtk::rowtopk_big_kernel<MODE, E, MASKED, TRACES>, a, s, smem, RTK_BIG_THREADS);
+}
+
+template <int MODE, int E, bool MASKED>
+int launch_big(const rtk::Args& a, cudaStream_t s) {
     if constexpr (MODE == rtk::kTrace) {
-        return launch_rows(rtk::rowtopk_pipe_kernel<MODE, Row, true>, a, s, smem);
+        return launch_big_kernel<MODE, E, MASKED, true>(a, s);
     } else {
         if ((a.iters != nullptr) != (a.reasons != nullptr))
             return fail(RTK_EINVAL, "iters and reasons must be both NULL or both non-NULL");
-        if (a.iters != nullptr) return launch_rows(rtk::rowtopk_pipe_kernel<MODE, Row, true>, a, s, smem);
-        return launch_rows(rtk::rowtopk_pipe_kernel<MODE, Row, false>, a, s, smem);
+        if (a.iters != nullptr) return launch_big_kernel<MODE, E, MASKED, true>(a, s);
+        return launch_big_kernel<MODE, E, MASKED, false>(a, s);
     }
 }
 
@@ -141,8 +152,8 @@ int launch_pair(const rtk::Args& a, cudaStream_t s) {
     if constexpr (MODE == rtk::kTrace || E > RTK_PAIR_MAX_E) {
         return fail(RTK_EINVAL, "internal: paired-row kernel not instantiated");
     } else {
-        // two selection staging buffers (32*E pairs each) per warp
-        const size_t smem = (size_t)(kThreads / 32) * 2 * 32 * E * 8;
+        // two selection staging buffers per warp
+        const size_t smem = (size_t)(kThreads / 32) * 2 * rtk::LaneRow<E, false>::kStageBytes;
         const bool wide = (reinterpret_cast<uintptr_t>(a.x) & 31) == 0 && a.ldx % 8 == 0;  // 256-bit loads
         if (a.m == 32 * E && wide) return launch_rows(rtk::rowtopk_pair_kernel<MODE, E, false, true>, a, s, smem);
         if (a.m == 32 * E) return launch_rows(rtk::rowtopk_pair_kernel<MODE, E, false, false>, a, s, smem);
@@ -153,15 +164,13 @@ int launch_pair(const rtk::Args& a, cudaStream_t s) {
 template <int MODE, int E>
 int launch_lane(const rtk::Args& a, cudaStream_t s) {
     if (pair_eligible<MODE, E>(a)) return launch_pair<MODE, E>(a, s);
-    // The cp.async row ring pays off where registers, not shared memory, limit
-    // occupancy (measured: +5% at M = 512; -48% at M = 1024, where the ring
-    // plus the staging buffer leave one CTA per SM).
-    if constexpr (E == 16) {
-        if (a.m == 32 * E) return launch_pipe_kernel<MODE, rtk::LaneRow<E, false, false>>(a, s);
-        return launch_pipe_kernel<MODE, rtk::LaneRow<E, true, false>>(a, s);
+    // Long rows: one register tile fed by a shared-memory ring (rtk_big.cuh).
+    if constexpr (E >= RTK_BIG_MIN_E) {
+        if (a.m == 32 * E) return launch_big<MODE, E, false>(a, s);
+        return launch_big<MODE, E, true>(a, s);
     }
-    // staging buffer: 32*E (value, index) pairs per warp (no selection in trace mode)
-    const size_t smem = MODE == rtk::kTrace ? 0 : (size_t)(kThreads / 32) * 32 * E * 8;
+    // staging buffer per warp: row copy + 32*E indices (no selection in trace mode)
+    const size_t smem = MODE == rtk::kTrace ? 0 : (size_t)(kThreads / 32) * rtk::LaneRow<E, false>::kStageBytes;
     const bool wide = (reinterpret_cast<uintptr_t>(a.x) & 31) == 0 && a.ldx % 8 == 0;  // 256-bit loads
     if (a.m == 32 * E && wide) return launch_row_kernel<MODE, rtk::LaneRow<E, false, true>>(a, s, smem);
     if (a.m == 32 * E) return launch_row_kernel<MODE, rtk::LaneRow<E, false, false>>(a, s, smem);
@@ -172,8 +181,8 @@ template <int MODE>
 int dispatch(const rtk::Args& a, cudaStream_t s) {
     const int m = a.m;
     const bool vec4 = (m % 4 == 0) && (a.ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
-#ifdef RTK_TUNE_E8  // tuning builds: only the M = 256 register tile (fast to compile)
-    if (m == 256 && vec4) return launch_lane<MODE, 8>(a, s);
+#ifdef RTK_TUNE_E  // tuning builds: only one register-tile width (fast to compile)
+    if (m <= 1024 && vec4 && (m + 127) / 128 * 4 == RTK_TUNE_E) return launch_lane<MODE, RTK_TUNE_E>(a, s);
     return launch_row_kernel<MODE, rtk::GlobalRow>(a, s, 0);
 #else
     if (m <= 1024 && vec4) {

@@ -177,6 +177,7 @@ template <int V, int C, bool MASKED>
 struct RegRow {
     static constexpr bool kStaged = true;  // selection goes through shared memory
     static constexpr int kPad = 0;         // staging holds exactly k entries
+    __host__ __device__ static constexpr unsigned stage_bytes(int k) { return (8u * (unsigned)k + 15u) & ~15u; }
     static constexpr int kV = V;
     static constexpr int kC = C;
     float v[C][V];
@@ -240,7 +241,7 @@ struct RegRow {
 
     // Stage the first k elements (ascending index) with v >= t into the
     // warp's shared-memory row buffer (_kernels.py:118-125, 205-212).
-    __device__ __forceinline__ void select_ge(float t, int k, unsigned sbase, int lane, int) const {
+    __device__ __forceinline__ unsigned select_ge(float t, int k, unsigned sbase, int lane, int) const {
         bool p[C][V];
 #pragma unroll
         for (int c = 0; c < C; ++c)
@@ -287,6 +288,7 @@ struct RegRow {
                 base += (int)((tot[c / 4] >> (8 * (c % 4))) & 0xffu);
             }
         }
+        return 0u;
     }
 
     // All elements >= t plus the first `need` elements of [lo, t), merged in
@@ -383,20 +385,39 @@ struct LaneRow {
         }
     }
 
-    // Row bytes of one pipeline slot (a warp's copy of one row).
-    static constexpr unsigned kRowBytes = 32u * E * 4u;
+    // Shared-memory image of a row (cp.async ring slots, the selection row
+    // copy): lane l's E values at l * kLaneStride.  The stride is padded to an
+    // odd number of 16-byte chunks, so the 8 lanes of each LDS.128/STS.128
+    // phase hit 8 distinct bank groups (an unpadded 4E-byte stride is an
+    // 8-way conflict at E = 32, 4-way at E = 16).
+    static constexpr unsigned kChunks = E / 4;
+    static constexpr unsigned kLaneStride = 16u * (kChunks | 1u);
+    static constexpr unsigned kRowBytes = 32u * kLaneStride;
+    // Unmasked rows with E dividing 128 are copied by the whole warp in
+    // 512-byte coalesced pieces (lane l: bytes [512 g + 16 l, +16) of the
+    // row), each 16-byte chunk sent to its owner lane's slot.
+    static constexpr bool kCoalescedStage = (128 % E == 0) && !MASKED;
 
-    // Issue this lane's share of row p into shared slot `slot` (every lane
-    // later reads back exactly the bytes it copied, so no cross-lane sync).
+    __device__ __forceinline__ static unsigned slot_offset(int lane) { return (unsigned)lane * kLaneStride; }
+
+    // Issue this lane's share of row p into shared slot `slot`.
     __device__ __forceinline__ static void stage_async(const float* __restrict__ p, int m, int lane, unsigned slot) {
-        const float* lp = p + lane * E;
-        const unsigned dst = slot + (unsigned)lane * E * 4u;
+        if constexpr (kCoalescedStage) {
+            // element e = 128 g + 4 lane lives in lane e / E, chunk (e % E) / 4
+            const unsigned dst = slot + (unsigned)(4 * lane / E) * kLaneStride + 16u * (unsigned)((4 * lane % E) / 4);
+            const float* src = p + 4 * lane;
 #pragma unroll
-        for (int g = 0; g < E / 4; ++g) cp_async16(dst + 16u * g, lp + 4 * g, valid(lane, 4 * g, m) ? 16u : 0u);
+            for (int g = 0; g < (int)kChunks; ++g) cp_async16(dst + g * (128u / E) * kLaneStride, src + 128 * g, 16u);
+        } else {
+            const float* lp = p + lane * E;
+            const unsigned dst = slot + slot_offset(lane);
+#pragma unroll
+            for (int g = 0; g < E / 4; ++g) cp_async16(dst + 16u * g, lp + 4 * g, valid(lane, 4 * g, m) ? 16u : 0u);
+        }
     }
 
     __device__ __forceinline__ void load_smem(unsigned slot, int m, int lane) {
-        const unsigned src = slot + (unsigned)lane * E * 4u;
+        const unsigned src = slot + slot_offset(lane);
 #pragma unroll
         for (int g = 0; g < E / 4; ++g) {
             const float4 q = lds128(src + 16u * g);
@@ -431,12 +452,19 @@ struct LaneRow {
         return MASKED ? max(0, min(E, m - lane * E)) : E;
     }
 
-    // Selection staging (per warp, kPad * 8 bytes of shared memory): the
-    // first half holds a copy of the row (lane l's E values at l*E), the
-    // second half the selected indices in output order.  Only indices are
-    // staged per element (one predicated STS.32 each, no register pairing);
-    // flush() looks the values up in the row copy.
-    static constexpr unsigned kIdxOff = 4u * 32u * E;
+    // Selection staging (per warp, kStageBytes of shared memory): a copy of
+    // the row (padded layout, see kLaneStride) followed by the selected
+    // indices in output order (32 E slots).  Only indices are staged per
+    // element (one predicated STS.32 each, no register pairing); flush()
+    // looks the values up in the row copy.
+    static constexpr unsigned kIdxOff = kRowBytes;
+    static constexpr unsigned kStageBytes = kRowBytes + 4u * 32u * E;
+    __host__ __device__ static constexpr unsigned stage_bytes(int) { return kStageBytes; }
+
+    // Shared-memory address of element i in the row copy at sbase.
+    __device__ __forceinline__ static unsigned copy_addr(unsigned sbase, unsigned i) {
+        return sbase + (i / E) * kLaneStride + 4u * (i % E);
+    }
 
     // A staged index is always < 32*E for NaN-free rows (#{v >= t} >= k);
     // NaN rows (reported as an error) may leave slots unwritten, so clamp
@@ -446,7 +474,7 @@ struct LaneRow {
     }
 
     __device__ __forceinline__ void stage_row(unsigned sbase, int lane) const {
-        const unsigned dst = sbase + (unsigned)lane * E * 4u;
+        const unsigned dst = sbase + slot_offset(lane);
 #pragma unroll
         for (int g = 0; g < E / 4; ++g)
             asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst + 16u * g), "f"(v[4 * g]),
@@ -473,19 +501,12 @@ struct LaneRow {
     // staging buffer holds 32*E entries, so no per-element cutoff is needed).
     // lane_hits: #{v >= t} in this lane, already known from the search pass
     // at t (the lane input of that pass's REDUX).
-    __device__ __forceinline__ void select_ge(float t, int, unsigned sbase, int lane, int lane_hits) const {
+    __device__ __forceinline__ unsigned select_ge(float t, int, unsigned sbase, int lane, int lane_hits) const {
         stage_row(sbase, lane);
         const unsigned cl = (unsigned)lane_hits;
         const unsigned excl = warp_incl_scan(cl) - cl;
-        unsigned addr = sbase + kIdxOff + 4u * excl;
-        const int i0 = lane * E;
-#pragma unroll
-        for (int q = 0; q < E; ++q) {
-            if (v[q] >= t) {
-                asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(i0 + q) : "memory");
-                addr += 4u;
-            }
-        }
+        stage_idx(t, sbase, lane, excl);
+        return 0u;
     }
 
     // All v >= t plus the first `need` elements of [lo, t), ascending index
@@ -525,11 +546,81 @@ struct LaneRow {
             int i;
             float x;
             asm volatile("ld.shared.b32 %0, [%1];" : "=r"(i) : "r"(sbase + kIdxOff + 4u * j) : "memory");
-            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(sbase + 4u * clamp_slot(i)) : "memory");
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(copy_addr(sbase, clamp_slot(i))) : "memory");
             ov[j] = x;
             oi[j] = i;
         }
         __syncwarp();
+    }
+};
+
+// Lane-contiguous tile with cut-off selection staging: only the first k
+// output positions are staged, as (value, index) pairs (8k bytes per warp,
+// flushed by flush_row), so long rows need little shared memory.  Used by
+// the big-row kernel (rtk_big.cuh).
+template <int E, bool MASKED>
+struct LaneRowCut : LaneRow<E, MASKED, false> {
+    using Base = LaneRow<E, MASKED, false>;
+    using Base::v;
+    static constexpr int kPad = 0;  // staging holds exactly k pairs (flush_row)
+    __host__ __device__ static constexpr unsigned stage_bytes(int k) { return (8u * (unsigned)k + 15u) & ~15u; }
+
+    // Staging addresses are computed a group of G slots ahead of the stores
+    // and all kept live until the group's stores have issued (folded into the
+    // returned sink), so ptxas cannot recycle one address register for the
+    // whole chain -- which would make every store wait for the previous
+    // STS to read its operands (a serial WAR chain through the MIO queue).
+    __device__ __forceinline__ unsigned select_ge(float t, int k, unsigned sbase, int lane, int lane_hits) const {
+        constexpr int G = (E % 8 == 0) ? 8 : 4;
+        const unsigned cl = (unsigned)lane_hits;
+        const unsigned excl = warp_incl_scan(cl) - cl;
+        unsigned addr = sbase + 8u * excl;
+        const unsigned aend = sbase + 8u * (unsigned)k;
+        const int i0 = lane * E;
+        unsigned sink = 0;
+#pragma unroll
+        for (int g = 0; g < E; g += G) {
+            unsigned ad[G];
+            bool p[G];
+#pragma unroll
+            for (int q = 0; q < G; ++q) {
+                const bool hit = v[g + q] >= t;
+                p[q] = hit && addr < aend;
+                ad[q] = addr;
+                addr += hit ? 8u : 0u;
+            }
+#pragma unroll
+            for (int q = 0; q < G; ++q)
+                if (p[q]) stage_put(ad[q], v[g + q], i0 + g + q);
+#pragma unroll
+            for (int q = 0; q < G; ++q) sink ^= ad[q];
+        }
+        return sink;
+    }
+
+    __device__ __forceinline__ void select_fill(float t, float lo, int need, int k, unsigned sbase, int lane) const {
+        bool pa[E], pb[E];
+        unsigned packed = 0;
+#pragma unroll
+        for (int q = 0; q < E; ++q) {
+            pa[q] = v[q] >= t;
+            pb[q] = (lo <= v[q]) && (v[q] < t);
+            packed += (pa[q] ? 1u : 0u) + (pb[q] ? 0x10000u : 0u);
+        }
+        const unsigned excl = warp_incl_scan(packed) - packed;
+        int ea = (int)(excl & 0xffffu), eb = (int)(excl >> 16);
+        const int i0 = lane * E;
+#pragma unroll
+        for (int q = 0; q < E; ++q) {
+            if (pa[q]) {
+                const int pos = ea + min(eb, need);
+                if (pos < k) stage_put(sbase + 8u * pos, v[q], i0 + q);
+                ++ea;
+            } else if (pb[q]) {
+                if (eb < need && ea + eb < k) stage_put(sbase + 8u * (ea + eb), v[q], i0 + q);
+                ++eb;
+            }
+        }
     }
 };
 
@@ -540,6 +631,7 @@ struct LaneRow {
 struct GlobalRow {
     static constexpr bool kStaged = false;  // selection stores straight to global
     static constexpr int kPad = 0;
+    __host__ __device__ static constexpr unsigned stage_bytes(int) { return 0u; }
     const float* __restrict__ p;
     int m;
 
@@ -565,8 +657,8 @@ struct GlobalRow {
         for (int e = threadIdx.x & 31; e < m; e += 32) cnt += (__ldg(p + e) >= t) ? 1 : 0;
         return (int)kLaneBias + cnt;
     }
-    __device__ __forceinline__ void select_ge(float t, int k, float* __restrict__ ov, int* __restrict__ oi,
-                                              int lane, int) const {
+    __device__ __forceinline__ unsigned select_ge(float t, int k, float* __restrict__ ov, int* __restrict__ oi,
+                                                  int lane, int) const {
         int base = 0;
         const unsigned lt = lanemask_lt();
         for (int c0 = 0; c0 < m && base < k; c0 += 32) {
@@ -581,6 +673,7 @@ struct GlobalRow {
             }
             base += __popc(b);
         }
+        return 0u;
     }
     __device__ __forceinline__ void select_fill(float t, float lo, int need, int k, float* __restrict__ ov,
                                                 int* __restrict__ oi, int lane) const {
@@ -730,13 +823,15 @@ __device__ __forceinline__ void early_loop(const Row& row, int kb, int max_iter,
 
 // Staged rows: LaneRow stages indices + a row copy (LaneRow::flush), RegRow
 // stages (value, index) pairs (flush_row).
+// dep: the staging sink ANDed with opaque_zero (0 at run time); adding it
+// to the flush addresses keeps the staging addresses live (LaneRowCut).
 template <class Row>
 __device__ __forceinline__ void flush_staged(unsigned sbase, int k, float* __restrict__ ov, int* __restrict__ oi,
-                                             int lane) {
+                                             int lane, unsigned dep = 0u) {
     if constexpr (Row::kPad > 0)
-        Row::flush(sbase, k, ov, oi, lane);
+        Row::flush(sbase + dep, k, ov, oi, lane);
     else
-        flush_row(sbase, k, ov, oi, lane);
+        flush_row(sbase + dep, k, ov, oi, lane);
 }
 
 struct NoHook {
@@ -770,11 +865,12 @@ __device__ __forceinline__ void select_exact(const Row& row, const Args& a, int 
         ca = warp_count(lane_t) - kCountBias;
     }
     if constexpr (Row::kStaged) {
+        unsigned sink = 0;
         if (ca >= k)
-            row.select_ge(t, k, sbase, lane, lane_t - (int)kLaneBias);
+            sink = row.select_ge(t, k, sbase, lane, lane_t - (int)kLaneBias);
         else
             row.select_fill(t, mn, k - ca, k, sbase, lane);
-        flush_staged<Row>(sbase, k, ov, oi, lane);
+        flush_staged<Row>(sbase, k, ov, oi, lane, sink & a.opaque_zero);
     } else {
         if (ca >= k)
             row.select_ge(t, k, ov, oi, lane, 0);
@@ -816,8 +912,8 @@ __device__ __forceinline__ void row_body(const Row& row, unsigned r, const Args&
             reason = kExitMaxIterReached;
         }
         if constexpr (Row::kStaged) {
-            row.select_ge(mn, k, sbase, lane, lane_mn - (int)kLaneBias);
-            flush_staged<Row>(sbase, k, ov, oi, lane);
+            const unsigned sink = row.select_ge(mn, k, sbase, lane, lane_mn - (int)kLaneBias);
+            flush_staged<Row>(sbase, k, ov, oi, lane, sink & a.opaque_zero);
         } else {
             row.select_ge(mn, k, ov, oi, lane, 0);
         }
@@ -891,12 +987,12 @@ template <int MODE, class Row, bool TRACES>
 __global__ void __launch_bounds__(RTK_CTA_THREADS, RTK_MIN_CTAS) rowtopk_kernel(Args a) {
     extern __shared__ __align__(16) float smem[];
     const int lane = threadIdx.x & 31;
-    const unsigned per_warp = Row::kPad ? (unsigned)Row::kPad : (unsigned)a.k;  // staging entries
+    const unsigned per_warp = MODE == kTrace ? 0u : Row::stage_bytes(a.k);  // staging bytes
     // The warp index is broadcast from lane 0 so ptxas can prove every row
     // loop below warp-uniform (no BRA.DIV convergence checks before the
     // REDUX/SHFL collectives, and uniform registers for the row bookkeeping).
     const int wid = __shfl_sync(kFull, (int)(threadIdx.x >> 5), 0);
-    const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem) + (unsigned)wid * 8u * per_warp;
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem) + (unsigned)wid * per_warp;
     const unsigned wpc = blockDim.x >> 5;
     const unsigned nw = gridDim.x * wpc;
     const unsigned n = (unsigned)a.n;
@@ -922,56 +1018,6 @@ __global__ void __launch_bounds__(RTK_CTA_THREADS, RTK_MIN_CTAS) rowtopk_kernel(
         if (!more2) break;
         r = r2;
     }
-}
-
-// Pipelined variant for the lane-contiguous tiles: each warp keeps a ring of
-// DEPTH row slots in shared memory filled by cp.async (LDGSTS) DEPTH grid
-// steps ahead, so DEPTH rows per warp are in flight instead of one register
-// tile.  Dynamic shared memory per warp: the selection staging buffer
-// (kPad pairs) followed by the DEPTH-slot row ring.
-#ifndef RTK_PIPE_DEPTH
-#define RTK_PIPE_DEPTH 3
-#endif
-template <int MODE, class Row, bool TRACES>
-__global__ void __launch_bounds__(RTK_CTA_THREADS, RTK_MIN_CTAS) rowtopk_pipe_kernel(Args a) {
-    constexpr int D = RTK_PIPE_DEPTH;
-    extern __shared__ __align__(16) float smem[];
-    const int lane = threadIdx.x & 31;
-    const int wid = __shfl_sync(kFull, (int)(threadIdx.x >> 5), 0);
-    const unsigned nwarps_cta = blockDim.x >> 5;
-    const unsigned base = (unsigned)__cvta_generic_to_shared(smem);
-    const unsigned sbase = base + (unsigned)wid * 8u * (unsigned)Row::kPad;
-    const unsigned ring = base + nwarps_cta * 8u * (unsigned)Row::kPad + (unsigned)wid * D * Row::kRowBytes;
-    const unsigned nw = gridDim.x * nwarps_cta;
-    const unsigned n = (unsigned)a.n;
-    unsigned r = blockIdx.x * nwarps_cta + (unsigned)wid;
-    if (r >= n) return;
-    const unsigned ldx_b = (unsigned)a.ldx * 4u;
-    const bool fp = a.eps_rel == 0.0;
-    // prologue: rows r, r+nw, ..., r+(D-1)nw
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-        const unsigned long long rd = (unsigned long long)r + (unsigned long long)d * nw;
-        if (rd < n) Row::stage_async(row_ptr(a.x, (unsigned)rd, ldx_b), a.m, lane, ring + d * Row::kRowBytes);
-        cp_async_commit();
-    }
-    unsigned slot = 0;
-    Row row;
-    for (;;) {
-        cp_async_wait<D - 1>();  // this row's group has landed
-        row.load_smem(ring + slot * Row::kRowBytes, a.m, lane);
-        const unsigned long long rpre = (unsigned long long)r + (unsigned long long)D * nw;
-        const bool refill = rpre < n;
-        const unsigned sl = ring + slot * Row::kRowBytes;
-        process_row<MODE, TRACES>(row, r, a, lane, sbase, fp, [&](unsigned) {
-            if (refill) Row::stage_async(row_ptr(a.x, (unsigned)rpre, ldx_b), a.m, lane, sl);
-            cp_async_commit();
-        });
-        if ((unsigned long long)r + nw >= n) break;
-        r += nw;
-        slot = slot + 1 == D ? 0 : slot + 1;
-    }
-    cp_async_wait<0>();
 }
 
 // k == M shortcut (_kernels.py:173-179): copy the row, indices 0..M-1, trace (0, DEGENERATE).

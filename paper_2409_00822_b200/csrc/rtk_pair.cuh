@@ -60,8 +60,8 @@ __device__ __forceinline__ void select_flush_pair(const Row& A, const Row& B, fl
             float xA, xB;
             asm volatile("ld.shared.b32 %0, [%1];" : "=r"(iA) : "r"(sA + Row::kIdxOff + 4u * lane) : "memory");
             asm volatile("ld.shared.b32 %0, [%1];" : "=r"(iB) : "r"(sB + Row::kIdxOff + 4u * lane) : "memory");
-            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xA) : "r"(sA + 4u * Row::clamp_slot(iA)) : "memory");
-            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xB) : "r"(sB + 4u * Row::clamp_slot(iB)) : "memory");
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xA) : "r"(Row::copy_addr(sA, Row::clamp_slot(iA))) : "memory");
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xB) : "r"(Row::copy_addr(sB, Row::clamp_slot(iB))) : "memory");
             ovA[lane] = xA;
             oiA[lane] = iA;
             ovB[lane] = xB;
@@ -76,8 +76,8 @@ __device__ __forceinline__ void select_flush_pair(const Row& A, const Row& B, fl
         float xA, xB;
         asm volatile("ld.shared.b32 %0, [%1];" : "=r"(iA) : "r"(sA + Row::kIdxOff + 4u * j) : "memory");
         asm volatile("ld.shared.b32 %0, [%1];" : "=r"(iB) : "r"(sB + Row::kIdxOff + 4u * j) : "memory");
-        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xA) : "r"(sA + 4u * Row::clamp_slot(iA)) : "memory");
-        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xB) : "r"(sB + 4u * Row::clamp_slot(iB)) : "memory");
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xA) : "r"(Row::copy_addr(sA, Row::clamp_slot(iA))) : "memory");
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xB) : "r"(Row::copy_addr(sB, Row::clamp_slot(iB))) : "memory");
         ovA[j] = xA;
         oiA[j] = iA;
         ovB[j] = xB;
@@ -204,8 +204,8 @@ __global__ void __launch_bounds__(RTK_CTA_THREADS, RTK_PAIR_MIN_CTAS) rowtopk_pa
     const int lane = threadIdx.x & 31;
     const int wid = __shfl_sync(kFull, (int)(threadIdx.x >> 5), 0);
     const unsigned wpc = blockDim.x >> 5;
-    const unsigned sA = (unsigned)__cvta_generic_to_shared(smem) + (unsigned)wid * 16u * (unsigned)Row::kPad;
-    const unsigned sB = sA + 8u * (unsigned)Row::kPad;
+    const unsigned sA = (unsigned)__cvta_generic_to_shared(smem) + (unsigned)wid * 2u * Row::kStageBytes;
+    const unsigned sB = sA + Row::kStageBytes;
     const unsigned nw = gridDim.x * wpc;
     const unsigned n = (unsigned)a.n;  // the host guarantees n + 2 nw < 2^32
     unsigned r = blockIdx.x * wpc + (unsigned)wid;

@@ -28,6 +28,9 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--shapes", default=None, help="comma list of M:k at N=2^20 (overrides the grid)")
+    ap.add_argument("--no-extra", action="store_true", help="skip the Reddit and C5 shapes")
+    ap.add_argument("--no-torch", action="store_true")
     args = ap.parse_args()
     peak, _ = peaks()
     torch.cuda.set_device(0)
@@ -51,8 +54,11 @@ def main():
     if args.quick:
         ms_list, ks = [256, 1024], [32, 128]
     shapes = [((1 << 20), m, k, "C3") for m in ms_list for k in ks]
-    shapes.append((232965, 256, 32, "C4 Reddit (238 MB input ~ L2 size: timed back to back)"))
-    shapes.append(((1 << 24), 512, 64, "C5 single-GPU share"))
+    if args.shapes:
+        shapes = [((1 << 20), int(t.split(":")[0]), int(t.split(":")[1]), "C3") for t in args.shapes.split(",")]
+    if not args.no_extra:
+        shapes.append((232965, 256, 32, "C4 Reddit (238 MB input ~ L2 size: timed back to back)"))
+        shapes.append(((1 << 24), 512, 64, "C5 single-GPU share"))
     g = torch.Generator(device="cuda").manual_seed(0)
     for n, m, k, tag in shapes:
         x = torch.randn((n, m), device="cuda", generator=g)
@@ -66,7 +72,7 @@ def main():
             rec[name] = {"ms": ms, "rows_per_s": n / (ms * 1e-3), "gb_per_s": bytes_ / (ms * 1e-3) / 1e9,
                          "frac": bytes_ / (ms * 1e-3) / 1e9 / peak}
             del outs
-        if n <= (1 << 20):
+        if n <= (1 << 20) and not args.no_torch:
             ms = time_ms(lambda: torch.topk(x, k, dim=1, sorted=True), max(3, steps // 5))
             rec["torch_topk_sorted"] = {"ms": ms, "rows_per_s": n / (ms * 1e-3)}
             rec["speedup_exact"] = ms / rec["exact"]["ms"]
