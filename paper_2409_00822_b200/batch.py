@@ -254,9 +254,140 @@ def _to_host(t, pinned: bool = True):
     return h
 
 
+# Host inputs are streamed through the device in row chunks of about this
+# many bytes: chunk i's H2D copy, chunk i-1's kernel and chunk i-2's D2H copy
+# run concurrently (copy engines in both directions + SMs).
+PIPELINE_CHUNK_BYTES = 64 << 20
+PIPELINE_SLOTS = 3  # device input buffers in the chunk ring
+
+
+def _launch_rows(x, k, search, vals, idx, iters, reasons, nan_word, stream):
+    """One C-ABI launch over the device matrix `x` (row slices of the full
+    outputs; iters/reasons may be None)."""
+    n, m = int(x.shape[0]), int(x.shape[1])
+    ldx = int(x.stride(0)) if n > 1 else m
+    ldo = int(vals.stride(0)) if n > 1 else int(k)
+    it_p = iters.data_ptr() if iters is not None else None
+    rs_p = reasons.data_ptr() if reasons is not None else None
+    if search.mode is SearchMode.EXACT:
+        _native.call("rtk_rowtopk_exact_f32", x.data_ptr(), n, m, ldx, int(k), float(search.epsilon_rel),
+                     int(search.hard_cap), vals.data_ptr(), idx.data_ptr(), ldo, it_p, rs_p,
+                     nan_word.data_ptr(), stream)
+    else:
+        _native.call("rtk_rowtopk_early_f32", x.data_ptr(), n, m, ldx, int(k), int(search.max_iter),
+                     vals.data_ptr(), idx.data_ptr(), ldo, it_p, rs_p, nan_word.data_ptr(), stream)
+
+
+def _host_pipeline(xh, k: int, search: SearchConfig, traces: bool):
+    """Row top-k of a host float32 matrix `xh` (CPU tensor, C-contiguous):
+    chunked H2D -> kernel -> D2H on three CUDA streams, results in pinned
+    host tensors.  Returns (vals, idx, iters, reasons, first_nan_row)."""
+    torch = _torch()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    n, m = int(xh.shape[0]), int(xh.shape[1])
+    rows = max(1, min(n, PIPELINE_CHUNK_BYTES // (4 * m)))
+    chunks = [(a, min(n, a + rows)) for a in range(0, n, rows)]
+    slots = min(PIPELINE_SLOTS, len(chunks))
+    pinned = xh.is_pinned()
+    # pageable input: stage through pinned chunk buffers (CPU copy overlaps the GPU work)
+    stage = [torch.empty((rows, m), dtype=torch.float32, pin_memory=True) for _ in range(2)] if not pinned else None
+    stage_free = [None, None]
+    xin = [torch.empty((rows, m), dtype=torch.float32, device=dev) for _ in range(slots)]
+    vals_d = torch.empty((n, k), dtype=torch.float32, device=dev)
+    idx_d = torch.empty((n, k), dtype=torch.int32, device=dev)
+    it_d = torch.zeros(n, dtype=torch.int32, device=dev) if traces else None
+    rs_d = torch.zeros(n, dtype=torch.int8, device=dev) if traces else None
+    nan_d = torch.empty(len(chunks), dtype=torch.int32, device=dev)
+    vals_h = torch.empty((n, k), dtype=torch.float32, pin_memory=True)
+    idx_h = torch.empty((n, k), dtype=torch.int32, pin_memory=True)
+    it_h = torch.empty(n, dtype=torch.int32, pin_memory=True) if traces else None
+    rs_h = torch.empty(n, dtype=torch.int8, pin_memory=True) if traces else None
+    nan_h = torch.empty(len(chunks), dtype=torch.int32, pin_memory=True)
+
+    s_comp = torch.cuda.current_stream(dev)
+    s_h2d = torch.cuda.Stream(dev)
+    s_d2h = torch.cuda.Stream(dev)
+    slot_free = [None] * slots  # kernel-done event of the last chunk that read each input slot
+    with torch.cuda.device(dev):
+        for i, (a, b) in enumerate(chunks):
+            sl, r = i % slots, b - a
+            src = xh[a:b]
+            if not pinned:
+                st = stage[i % 2]
+                if stage_free[i % 2] is not None:
+                    stage_free[i % 2].synchronize()  # its previous H2D has drained
+                st[:r].copy_(src)
+                src = st[:r]
+            with torch.cuda.stream(s_h2d):
+                if slot_free[sl] is not None:
+                    s_h2d.wait_event(slot_free[sl])
+                xin[sl][:r].copy_(src, non_blocking=True)
+                h2d_done = torch.cuda.Event()
+                h2d_done.record(s_h2d)
+                if not pinned:
+                    stage_free[i % 2] = h2d_done
+            s_comp.wait_event(h2d_done)
+            _launch_rows(xin[sl][:r], k, search, vals_d[a:b], idx_d[a:b],
+                         it_d[a:b] if traces else None, rs_d[a:b] if traces else None,
+                         nan_d[i:i + 1], s_comp.cuda_stream)
+            done = torch.cuda.Event()
+            done.record(s_comp)
+            slot_free[sl] = done
+            with torch.cuda.stream(s_d2h):
+                s_d2h.wait_event(done)
+                vals_h[a:b].copy_(vals_d[a:b], non_blocking=True)
+                idx_h[a:b].copy_(idx_d[a:b], non_blocking=True)
+                if traces:
+                    it_h[a:b].copy_(it_d[a:b], non_blocking=True)
+                    rs_h[a:b].copy_(rs_d[a:b], non_blocking=True)
+        with torch.cuda.stream(s_d2h):
+            nan_h.copy_(nan_d, non_blocking=True)
+        s_d2h.synchronize()
+    first_nan = -1
+    for i, (a, _) in enumerate(chunks):
+        w = int(nan_h[i])
+        if w != -1:
+            first_nan = a + (w & 0xFFFFFFFF)
+            break
+    return vals_h, idx_h, it_h, rs_h, first_nan
+
+
+def _host_tensor(matrix):
+    """Host input as a C-contiguous float32 CPU tensor, validated like
+    as_matrix (batch.py:30-36); pinned tensors are kept as they are."""
+    torch = _torch()
+    if _is_torch(matrix) and matrix.dim() == 2 and matrix.dtype == torch.float32 and not matrix.is_cuda:
+        t = matrix if matrix.is_contiguous() else matrix.contiguous()
+        if t.numel() == 0:
+            raise EmptyRowError(f"matrix must be at least 1 x 1, got {tuple(t.shape)}")
+        return t
+    return torch.from_numpy(_host_matrix(matrix))
+
+
 def batch_topk(matrix, cfg: BatchConfig) -> BatchResult:
     """Run the configured top-k search over every row (batch.py:105-142) on the
-    current CUDA device."""
+    current CUDA device.  Host inputs stream through the device in row chunks
+    (H2D, kernel and D2H overlapped; results come back as numpy arrays);
+    CUDA tensors are processed in place (results stay on their device)."""
+    if not (_is_torch(matrix) and matrix.is_cuda):
+        _require_cuda()
+        xh = _host_tensor(matrix)
+        k = int(cfg.k)
+        m = int(xh.shape[1])
+        if k < 1 or k > m:
+            r = _DeviceMatrix(xh).first_nan_row()  # NaN is reported before the k-range error (batch.py:107-111)
+            if r >= 0:
+                raise NaNInputError(f"matrix contains NaN (first offending row: {r})")
+            raise KOutOfRangeError(f"k must be in [1, {m}], got {k}")
+        resolve_workers(cfg.workers)
+        vals, idx, iters, reasons, r = _host_pipeline(xh, k, cfg.search, cfg.collect_traces)
+        if r >= 0:
+            raise NaNInputError(f"matrix contains NaN (first offending row: {r})")
+        outs = [o.numpy() if o is not None else None for o in (vals, idx, iters, reasons)]
+        if cfg.collect_traces:
+            return BatchResult(*outs)
+        return BatchResult(outs[0], outs[1])
+
     dm = _DeviceMatrix(matrix)
     k = int(cfg.k)
     if k < 1 or k > dm.m:
@@ -268,19 +399,9 @@ def batch_topk(matrix, cfg: BatchConfig) -> BatchResult:
 
     nan_word = dm._new_nan_word()
     vals, idx, iters, reasons = dm.launch_topk(k, cfg.search, cfg.collect_traces, nan_word=nan_word)
-    if dm.host:
-        outs = [_to_host(t) for t in (vals, idx, iters, reasons)]
-        nan_h = _to_host(nan_word)
-        _torch().cuda.current_stream(dm.device).synchronize()
-        r = int(nan_h.item())
-    else:
-        outs = [vals, idx, iters, reasons]
-        r = int(nan_word.item())
+    r = int(nan_word.item())
     if r != -1:
         raise NaNInputError(f"matrix contains NaN (first offending row: {r & 0xFFFFFFFF})")
-    if dm.host:
-        outs = [o.numpy() if o is not None else None for o in outs]
-    vals, idx, iters, reasons = outs
     if cfg.collect_traces:
         return BatchResult(vals, idx, iters, reasons)
     return BatchResult(vals, idx)
