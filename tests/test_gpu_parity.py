@@ -111,6 +111,10 @@ def test_reference_digests_at_baseline_sizes(limit):
         t, r = res.trace_iterations.cpu().numpy(), res.trace_reasons.cpu().numpy()
         assert h16(v, i) == c["out"], c
         assert h16(t, r) == c["tr"], c
+        # the hot path (no traces: paired-row / long-row kernels)
+        cfg = rtk.BatchConfig(k=c["k"], search=_search(c["mode"], c["max_iter"], c["eps_rel"]))
+        res = rtk.batch_topk(mats[key], cfg)
+        assert h16(res.values.cpu().numpy(), res.indices.cpu().numpy()) == c["out"], ("no traces", c)
         checked += 1
     assert checked > 0
 
@@ -131,6 +135,104 @@ def test_random_shapes_vs_oracle(oracle_lib):
         want = oracle_lib.ref_batch(x, k, mode, max_iter=mi, eps_rel=eps, hard_cap=cap)
         res = rtk.batch_topk(x, rtk.BatchConfig(k=k, search=_search(mode, mi, eps, cap), collect_traces=True))
         _check(res, *want, (trial, n, m, k, mode, mi, eps, cap, style))
+        res = rtk.batch_topk(x, rtk.BatchConfig(k=k, search=_search(mode, mi, eps, cap)))
+        assert np.array_equal(res.indices, want[1]), ("no traces", trial, n, m, k, mode)
+        assert np.array_equal(_bits(res.values), _bits(want[0])), ("no traces", trial, n, m, k, mode)
+
+
+def _mixed_rows(rng, n, m):
+    """Rows that take every branch of the fast kernels when processed in
+    pairs: N(0,1), tie-heavy styles, constant (degenerate), +-inf, values
+    beyond 2^126 (general midpoint), subnormals, duplicated maxima, +-0."""
+    kinds = ["normal"] * 6 + ["small-int", "quantized", "constant", "inf", "huge", "tiny", "dupmax", "zeros"]
+    rows = []
+    for r in range(n):
+        kind = kinds[int(rng.integers(len(kinds)))]
+        if kind in ("normal", "small-int", "quantized", "constant"):
+            row = random_row(rng, m, kind)
+        elif kind == "inf":
+            row = rng.standard_normal(m).astype(np.float32)
+            row[rng.integers(m, size=max(1, m // 50))] = np.float32(np.inf) if r % 2 else np.float32(-np.inf)
+        elif kind == "huge":
+            row = np.clip(rng.standard_normal(m) * 1.5e38, -3.4e38, 3.4e38).astype(np.float32)
+        elif kind == "tiny":
+            row = (rng.integers(-20, 21, m) * np.float32(1e-45)).astype(np.float32)
+        elif kind == "dupmax":
+            row = rng.standard_normal(m).astype(np.float32)
+            row[rng.integers(m, size=max(2, m // 8))] = row.max()
+        else:
+            row = np.where(rng.integers(2, size=m) == 1, np.float32(-0.0), np.float32(0.0)).astype(np.float32)
+            row[rng.integers(m, size=3)] = rng.standard_normal(3).astype(np.float32)
+        rows.append(row)
+    return np.stack(rows)
+
+
+@pytest.mark.parametrize("m", [4, 8, 100, 128, 200, 256, 260, 384, 500, 512, 640, 768, 1000, 1024])
+def test_fast_paths_mixed_rows_vs_oracle(oracle_lib, m):
+    """The no-trace hot paths (paired-row kernel for M <= 256, long-row kernel
+    above, masked and unmasked tiles) on odd row counts mixing fast-loop rows
+    with rows that need the general per-row path, vs the oracle; then the
+    trace path on the same input."""
+    rng = np.random.default_rng(1000 + m)
+    n = 777 if m <= 256 else 333
+    x = _mixed_rows(rng, n, m)
+    ks = sorted({1, min(7, m), min(32, m), max(1, m // 3), max(1, m - 1)})
+    searches = [("exact", 4, 0.0, 64), ("exact", 4, 0.0, 7), ("exact", 4, 1e-4, 64), ("early", 2, 0.0, 64),
+                ("early", 4, 0.0, 64), ("early", 9, 0.0, 64)]
+    for k in ks:
+        for mode, mi, eps, cap in searches:
+            want = oracle_lib.ref_batch(x, k, mode, max_iter=mi, eps_rel=eps, hard_cap=cap)
+            ctx = (m, k, mode, mi, eps, cap)
+            res = rtk.batch_topk(x, rtk.BatchConfig(k=k, search=_search(mode, mi, eps, cap)))
+            assert np.array_equal(res.indices, want[1]), ctx
+            assert np.array_equal(_bits(res.values), _bits(want[0])), ctx
+            xd = torch.from_numpy(x).cuda()
+            res = rtk.batch_topk(xd, rtk.BatchConfig(k=k, search=_search(mode, mi, eps, cap), collect_traces=True))
+            _check(res, *want, ctx)
+
+
+def test_fast_paths_many_grid_steps_vs_oracle(oracle_lib):
+    """Enough rows that every warp of the persistent grid takes many pair /
+    ring steps (and an odd tail), device-resident, no traces; sampled rows vs
+    the oracle."""
+    g = torch.Generator(device="cuda").manual_seed(11)
+    for n, m, k in ((300_001, 256, 32), (300_001, 128, 16), (120_001, 1024, 64), (150_001, 512, 64),
+                    (100_003, 768, 128)):
+        x = torch.randn(n, m, device="cuda", generator=g)
+        rows = torch.tensor([0, 1, 2, 3, n // 3, n // 2 + 1, n - 4, n - 3, n - 2, n - 1], device="cuda")
+        xs = x[rows].cpu().numpy()
+        for search, mode in ((rtk.SearchConfig.exact(), "exact"), (rtk.SearchConfig.early_stop(4), "early")):
+            res = rtk.batch_topk(x, rtk.BatchConfig(k=k, search=search))
+            v, i, _, _ = oracle_lib.ref_batch(xs, k, mode, max_iter=4)
+            assert np.array_equal(res.indices[rows].cpu().numpy(), i), (n, m, k, mode)
+            assert np.array_equal(_bits(res.values[rows].cpu().numpy()), _bits(v)), (n, m, k, mode)
+        del x
+    torch.cuda.empty_cache()
+
+
+def test_host_pipeline_chunks_match_device_path(monkeypatch):
+    """The chunked H2D -> kernel -> D2H host path (small chunks, pinned and
+    pageable inputs, traces on and off) equals the device-resident launch;
+    NaN rows are reported with their global row index."""
+    from paper_2409_00822_b200 import batch as B
+
+    monkeypatch.setattr(B, "PIPELINE_CHUNK_BYTES", 256 * 1024)
+    x = np.random.default_rng(5).standard_normal((10_007, 256), dtype=np.float32)
+    for search in (rtk.SearchConfig.exact(), rtk.SearchConfig.early_stop(3)):
+        for traces in (False, True):
+            cfg = rtk.BatchConfig(k=20, search=search, collect_traces=traces)
+            want = rtk.batch_topk(torch.from_numpy(x).cuda(), cfg)
+            for host in (x, torch.from_numpy(x).pin_memory()):
+                got = rtk.batch_topk(host, cfg)
+                assert np.array_equal(got.indices, want.indices.cpu().numpy())
+                assert np.array_equal(_bits(got.values), _bits(want.values.cpu().numpy()))
+                if traces:
+                    assert np.array_equal(got.trace_iterations, want.trace_iterations.cpu().numpy())
+                    assert np.array_equal(got.trace_reasons, want.trace_reasons.cpu().numpy())
+    x[7000, 3] = np.nan
+    x[9000, 3] = np.nan
+    with pytest.raises(rtk.NaNInputError, match="first offending row: 7000\\)"):
+        rtk.batch_topk(x, rtk.BatchConfig(k=5))
 
 
 def test_single_row_api_matches_batch_rows():
