@@ -393,26 +393,20 @@ struct LaneRow {
     static constexpr unsigned kChunks = E / 4;
     static constexpr unsigned kLaneStride = 16u * (kChunks | 1u);
     static constexpr unsigned kRowBytes = 32u * kLaneStride;
-    // Unmasked rows with E dividing 128 are copied by the whole warp in
-    // 512-byte coalesced pieces (lane l: bytes [512 g + 16 l, +16) of the
-    // row), each 16-byte chunk sent to its owner lane's slot.
-    static constexpr bool kCoalescedStage = (128 % E == 0) && !MASKED;
-
+    // The warp copies a row in 512-byte coalesced pieces (lane l: bytes
+    // [512 g + 16 l, +16) of the row) and sends each 16-byte chunk to its
+    // owner lane's slot: element e = 128 g + 4 l lives in lane e / E, chunk
+    // (e % E) / 4 (constant divisors; for E | 128 the offsets are
+    // base + g * const).  Chunks past M are zero-filled (M % 4 == 0 here).
     __device__ __forceinline__ static unsigned slot_offset(int lane) { return (unsigned)lane * kLaneStride; }
 
-    // Issue this lane's share of row p into shared slot `slot`.
     __device__ __forceinline__ static void stage_async(const float* __restrict__ p, int m, int lane, unsigned slot) {
-        if constexpr (kCoalescedStage) {
-            // element e = 128 g + 4 lane lives in lane e / E, chunk (e % E) / 4
-            const unsigned dst = slot + (unsigned)(4 * lane / E) * kLaneStride + 16u * (unsigned)((4 * lane % E) / 4);
-            const float* src = p + 4 * lane;
+        const float* src = p + 4 * lane;
 #pragma unroll
-            for (int g = 0; g < (int)kChunks; ++g) cp_async16(dst + g * (128u / E) * kLaneStride, src + 128 * g, 16u);
-        } else {
-            const float* lp = p + lane * E;
-            const unsigned dst = slot + slot_offset(lane);
-#pragma unroll
-            for (int g = 0; g < E / 4; ++g) cp_async16(dst + 16u * g, lp + 4 * g, valid(lane, 4 * g, m) ? 16u : 0u);
+        for (int g = 0; g < (int)kChunks; ++g) {
+            const unsigned e = 128u * g + 4u * (unsigned)lane;
+            const unsigned dst = slot + (e / E) * kLaneStride + 16u * ((e % E) / 4u);
+            cp_async16(dst, src + 128 * g, (!MASKED || (int)e < m) ? 16u : 0u);
         }
     }
 

@@ -11,6 +11,7 @@ def main():
     d, mode = sys.argv[1], sys.argv[2]
     rows = float(sys.argv[3]) if len(sys.argv) > 3 else float(1 << 20)
     det = open(f"{d}/prof_{mode}_details.txt").read()
+    print(f"  capture {mode}: {rows:.0f} rows")
     for key in ("Duration", "DRAM Throughput", "Issue Slots Busy", "Executed Ipc Active", "Registers Per Thread",
                 "Achieved Occupancy", "No Eligible", "Eligible Warps Per Scheduler"):
         m = re.search(rf"^\s*{re.escape(key)}\s+(\S+)\s+(\S+)", det, re.M)
