@@ -21,8 +21,8 @@
  *     of the first row holding a NaN.  The caller reads it after the stream
  *     completes and raises NaNInputError (rows with NaN get unspecified output).
  *
- * Row layout: x is row-major, row r starts at x + r*ldx (ldx >= m).  Outputs
- * row r start at vals + r*ldo / idx + r*ldo (ldo >= k).  Exactly k values and
+ * Row layout: x is row-major, row r starts at x + r*ldx (m <= ldx < 2^30).
+ * Outputs row r start at vals + r*ldo / idx + r*ldo (k <= ldo < 2^30); n < 2^32 - 1.  Exactly k values and
  * k int32 indices are written per row, indices ascending, values bit copies
  * of x (_kernels.py:106-146).  iters (int32) / reasons (int8, ExitReason codes
  * 1..5, _kernels.py:19-23) are per-row traces; both NULL turns trace
