@@ -51,6 +51,10 @@ extern "C" {
 #define RTK_OK 0
 #define RTK_EINVAL 1
 #define RTK_ECUDA 2
+#define RTK_EIO 3     /* file open/read/write failed (rtk_topk_file_f32) */
+#define RTK_EFORMAT 4 /* bad magic or unsupported format version */
+#define RTK_ETRUNC 5  /* file shorter than its header declares, or empty payload */
+#define RTK_ENAN 6    /* the matrix holds a NaN (first offending row reported) */
 
 #define RTK_EXIT_COUNT_EQUALS_K 1
 #define RTK_EXIT_INTERVAL_BELOW_EPSILON 2
@@ -99,6 +103,25 @@ RTK_API int rtk_row_min_max_f32(const float *x, int64_t n, int64_t m, int64_t ld
                         float *maxs, void *stream);
 RTK_API int rtk_count_ge_f32(const float *x, int64_t n, int64_t m, int64_t ldx, const float *thres,
                      int32_t *counts, void *stream);
+
+/* File-level job: RTKM matrix file -> row top-k on the current CUDA device
+ * -> RTKR result file, streamed in chunks of `chunk_rows` rows (0 = ~64 MB):
+ * pread into pinned host buffers, H2D, kernel, D2H and pwrite of consecutive
+ * chunks overlap (three CUDA streams, double-buffered).  Replaces the
+ * reference's load_matrix -> batch_topk -> save_result chain
+ * (io.py:46-78, batch.py:105-142; formats SPEC.md:239): magic "RTKM"/"RTKR",
+ * u32 version 1, u64 n_rows, u64 n_cols (= k for results), little-endian
+ * binary32 payload; the result holds all values then all indices (u32).
+ * mode: 0 exact (eps_rel, hard_cap), 1 early stop (max_iter).
+ * Unlike the operator entry points this call allocates (device + pinned
+ * buffers) and synchronises.  Error precedence follows the reference:
+ * RTK_EIO / RTK_EFORMAT / RTK_ETRUNC for the input file, then RTK_ENAN
+ * (dims[2] = first row holding a NaN; the partial output is removed), then
+ * RTK_EINVAL for k outside [1, n_cols].  dims (nullable) receives
+ * {n_rows, n_cols, first_nan_row or -1}. */
+RTK_API int rtk_topk_file_f32(const char *matrix_path, const char *result_path, int32_t k, int32_t mode,
+                      double eps_rel, int32_t hard_cap, int32_t max_iter, int64_t chunk_rows,
+                      int64_t *dims);
 
 /* Thread-local description of the last non-OK return. */
 RTK_API const char *rtk_last_error(void);

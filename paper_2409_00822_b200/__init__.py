@@ -31,6 +31,7 @@ from .errors import (  # noqa: F401
     TruncatedFileError,
     VerificationError,
 )
+from .io import load_matrix, load_result, save_matrix, save_result, topk_file  # noqa: F401
 from .select import (  # noqa: F401
     DEFAULT_HARD_CAP,
     DEFAULT_MAX_ITER,
@@ -52,5 +53,6 @@ __all__ = [
     "DimensionMismatchError", "EmptyRowError", "ExitReason", "KOutOfRangeError", "NaNInputError",
     "REGISTER_COLS_LIMIT", "RowTopKError", "SOFT_COLS_LIMIT", "SearchConfig", "SearchMode", "SearchTrace",
     "TopKResult", "as_matrix", "as_row", "batch_topk", "chunk_ranges", "count_ge", "early_stop_topk",
-    "exact_topk", "exact_trace", "min_max", "oracle_topk", "resolve_workers",
+    "exact_topk", "exact_trace", "min_max", "oracle_topk", "resolve_workers", "load_matrix", "load_result",
+    "save_matrix", "save_result", "topk_file",
 ]

@@ -14,15 +14,16 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SO = os.path.join(PKG, "librtk.so")
-SOURCES = [os.path.join(CSRC, "rtk_capi.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "rtk_kernels.cuh"), os.path.join(ROOT, "include", "rtk.h")]
+SOURCES = [os.path.join(CSRC, "rtk_capi.cu"), os.path.join(CSRC, "rtk_io.cpp")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("rtk_kernels.cuh", "rtk_pair.cuh", "rtk_big.cuh")] + \
+    [os.path.join(ROOT, "include", "rtk.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "-fmad=false", "-ftz=false", "-prec-div=true", "-prec-sqrt=true",
     "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-    "-shared",
+    "-shared", "-Xcompiler", "-pthread",
 ]
 
 

@@ -13,7 +13,7 @@ import threading
 from ._build import SO
 from .errors import DeviceError
 
-RTK_OK, RTK_EINVAL, RTK_ECUDA = 0, 1, 2
+RTK_OK, RTK_EINVAL, RTK_ECUDA, RTK_EIO, RTK_EFORMAT, RTK_ETRUNC, RTK_ENAN = 0, 1, 2, 3, 4, 5, 6
 
 _lock = threading.Lock()
 _lib = None
@@ -33,6 +33,8 @@ SIGNATURES = {
     "rtk_nan_scan_f32": (ctypes.c_int, [_p, _i64, _i64, _i64, _p, _p]),
     "rtk_row_min_max_f32": (ctypes.c_int, [_p, _i64, _i64, _i64, _p, _p, _p]),
     "rtk_count_ge_f32": (ctypes.c_int, [_p, _i64, _i64, _i64, _p, _p, _p]),
+    "rtk_topk_file_f32": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, _i32, _i32, ctypes.c_double, _i32, _i32,
+                                         _i64, _p]),
     "rtk_last_error": (ctypes.c_char_p, []),
     "rtk_version": (ctypes.c_int, []),
     "rtk_launch_shape": (ctypes.c_int, [_i64, _i32, _i32, _p, _p, _p]),
@@ -65,6 +67,10 @@ def check(rc: int, what: str) -> None:
     if rc != RTK_OK:
         msg = load().rtk_last_error().decode(errors="replace")
         raise DeviceError(f"{what} failed (rc={rc}): {msg}")
+
+
+def last_error() -> str:
+    return load().rtk_last_error().decode(errors="replace")
 
 
 def call(name: str, *args) -> None:

@@ -21,12 +21,22 @@ namespace {
 
 thread_local char g_err[512] = "";
 
-int fail(int code, const char* fmt, ...) {
+}  // namespace
+
+// Library-internal (hidden): record the thread-local error message.
+int rtk_fail(int code, const char* fmt, ...) {
     va_list ap;
     va_start(ap, fmt);
     vsnprintf(g_err, sizeof g_err, fmt, ap);
     va_end(ap);
     return code;
+}
+
+namespace {
+
+template <class... T>
+int fail(int code, const char* fmt, T... args) {
+    return rtk_fail(code, fmt, args...);
 }
 
 #ifndef RTK_BIG_MIN_E
