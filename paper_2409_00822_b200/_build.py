@@ -9,21 +9,24 @@ from __future__ import annotations
 import os
 import shutil
 import subprocess
+import tempfile
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SO = os.path.join(PKG, "librtk.so")
-SOURCES = [os.path.join(CSRC, "rtk_capi.cu"), os.path.join(CSRC, "rtk_io.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("rtk_kernels.cuh", "rtk_pair.cuh", "rtk_big.cuh")] + \
-    [os.path.join(ROOT, "include", "rtk.h")]
+# one translation unit per mode so nvcc compiles the kernel instantiations in parallel
+SOURCES = [os.path.join(CSRC, f) for f in ("rtk_dispatch_exact.cu", "rtk_dispatch_early.cu", "rtk_dispatch_trace.cu",
+                                           "rtk_capi.cu", "rtk_io.cpp")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("rtk_kernels.cuh", "rtk_pair.cuh", "rtk_big.cuh",
+                                                  "rtk_dispatch.cuh")] + [os.path.join(ROOT, "include", "rtk.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "-fmad=false", "-ftz=false", "-prec-div=true", "-prec-sqrt=true",
     "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-    "-shared", "-Xcompiler", "-pthread",
+    "-Xcompiler", "-pthread",
 ]
 
 
@@ -48,9 +51,23 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, ex
     if out is None and not force and not needs_build():
         return SO
     tmp = target + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, *(extra or []), "-I", os.path.join(ROOT, "include"), "-o", tmp, *SOURCES]
-    if verbose:
-        print(" ".join(cmd), flush=True)
-    subprocess.run(cmd, check=True)
+    inc = ["-I", os.path.join(ROOT, "include")]
+    with tempfile.TemporaryDirectory(prefix="rtk_build_") as objdir:
+        procs, objs = [], []
+        for src in SOURCES:
+            obj = os.path.join(objdir, os.path.basename(src) + ".o")
+            cmd = [nvcc(), *NVCC_FLAGS, *(extra or []), *inc, "-c", "-o", obj, src]
+            if verbose:
+                print(" ".join(cmd), flush=True)
+            procs.append((subprocess.Popen(cmd), cmd))
+            objs.append(obj)
+        failed = [cmd for p, cmd in procs if p.wait() != 0]
+        if failed:
+            raise subprocess.CalledProcessError(1, failed[0])
+        link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-pthread",
+                "-o", tmp, *objs]
+        if verbose:
+            print(" ".join(link), flush=True)
+        subprocess.run(link, check=True)
     os.replace(tmp, target)
     return target

@@ -1,0 +1,176 @@
+// rtk_dispatch.cuh -- kernel selection and launch for one mode (included by
+// the per-mode translation units rtk_dispatch_{exact,early,trace}.cu, which
+// nvcc compiles in parallel).  Chooses the tile / kernel for (M, alignment,
+// traces), sizes the persistent grid from the occupancy of that
+// instantiation and launches on the caller's stream.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "rtk.h"
+#include "rtk_big.cuh"
+#include "rtk_kernels.cuh"
+#include "rtk_pair.cuh"
+
+// library-internal (rtk_capi.cu)
+int rtk_fail(int code, const char* fmt, ...);
+int rtk_device_sms();
+int rtk_ctas_per_sm(const void* kernel, size_t smem, int threads);
+int rtk_dispatch_exact(const rtk::Args& a, cudaStream_t s);
+int rtk_dispatch_early(const rtk::Args& a, cudaStream_t s);
+int rtk_dispatch_trace(const rtk::Args& a, cudaStream_t s);
+
+namespace rtk_dispatch {
+
+template <class... T>
+int fail(int code, const char* fmt, T... args) {
+    return rtk_fail(code, fmt, args...);
+}
+
+#ifndef RTK_BIG_MIN_E
+#define RTK_BIG_MIN_E 12  // smallest elements-per-lane tile routed to the long-row kernel
+#endif
+#ifndef RTK_PAIR_MAX_E
+#define RTK_PAIR_MAX_E 8  // largest elements-per-lane tile routed to the paired-row kernel
+#endif
+constexpr int kThreads = RTK_CTA_THREADS;  // threads per CTA of the row kernels
+constexpr int kFlatThreads = 256;         // threads per CTA of the elementwise kernels
+
+
+template <class K>
+int launch_rows(K kernel, const rtk::Args& a, cudaStream_t s, size_t smem, int threads = kThreads) {
+    const long long warps_needed = a.n;
+    const long long blocks_needed = (warps_needed + (threads / 32) - 1) / (threads / 32);
+    long long grid = (long long)rtk_device_sms() * rtk_ctas_per_sm(reinterpret_cast<const void*>(kernel), smem, threads);
+    if (grid > blocks_needed) grid = blocks_needed;
+    if (grid < 1) grid = 1;
+    kernel<<<(unsigned)grid, threads, smem, s>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(RTK_ECUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+    return RTK_OK;
+}
+
+// Launch one row-kernel instantiation; traces are a template flag so the
+// common no-trace launch carries no per-row trace stores.
+template <int MODE, class Row>
+int launch_row_kernel(const rtk::Args& a, cudaStream_t s, size_t smem) {
+    if constexpr (MODE == rtk::kTrace) {
+        return launch_rows(rtk::rowtopk_kernel<MODE, Row, true>, a, s, smem);
+    } else {
+        if ((a.iters != nullptr) != (a.reasons != nullptr))
+            return fail(RTK_EINVAL, "iters and reasons must be both NULL or both non-NULL");
+        if (a.iters != nullptr) return launch_rows(rtk::rowtopk_kernel<MODE, Row, true>, a, s, smem);
+        return launch_rows(rtk::rowtopk_kernel<MODE, Row, false>, a, s, smem);
+    }
+}
+
+template <int MODE, int V, int C>
+int launch_reg(const rtk::Args& a, cudaStream_t s) {
+    // staging buffer: k (value, index) pairs per warp (no selection in trace mode)
+    const size_t smem = MODE == rtk::kTrace ? 0 : (size_t)(kThreads / 32) * rtk::RegRow<V, C, false>::stage_bytes(a.k);
+    if (a.m == C * 32 * V) return launch_row_kernel<MODE, rtk::RegRow<V, C, false>>(a, s, smem);
+    return launch_row_kernel<MODE, rtk::RegRow<V, C, true>>(a, s, smem);
+}
+
+// Long rows (rtk_big.cuh): one register tile, cp.async ring, k-pair staging.
+template <int MODE, int E, bool MASKED, bool TRACES>
+int launch_big_kernel(const rtk::Args& a, cudaStream_t s) {
+    using Row = rtk::LaneRowCut<E, MASKED>;
+    constexpr int wpc = RTK_BIG_THREADS / 32;
+    const size_t smem = (size_t)wpc * (Row::stage_bytes(a.k) + RTK_BIG_DEPTH * Row::kRowBytes);
+    return launch_rows(rtk::rowtopk_big_kernel<MODE, E, MASKED, TRACES>, a, s, smem, RTK_BIG_THREADS);
+}
+
+template <int MODE, int E, bool MASKED>
+int launch_big(const rtk::Args& a, cudaStream_t s) {
+    if constexpr (MODE == rtk::kTrace) {
+        return launch_big_kernel<MODE, E, MASKED, true>(a, s);
+    } else {
+        if ((a.iters != nullptr) != (a.reasons != nullptr))
+            return fail(RTK_EINVAL, "iters and reasons must be both NULL or both non-NULL");
+        if (a.iters != nullptr) return launch_big_kernel<MODE, E, MASKED, true>(a, s);
+        return launch_big_kernel<MODE, E, MASKED, false>(a, s);
+    }
+}
+
+// Paired-row kernel (rtk_pair.cuh): launches without traces; exact mode
+// only with eps_rel == 0.
+template <int MODE, int E>
+bool pair_eligible(const rtk::Args& a) {
+    if constexpr (MODE == rtk::kTrace || E > RTK_PAIR_MAX_E) {
+        return false;
+    } else {
+        if (a.iters != nullptr || a.reasons != nullptr) return false;
+        if (a.n >= 0xffff0000LL) return false;  // 32-bit row cursors: n + 2 * (warps in the grid) < 2^32
+        return MODE == rtk::kEarly || a.eps_rel == 0.0;
+    }
+}
+
+template <int MODE, int E>
+int launch_pair(const rtk::Args& a, cudaStream_t s) {
+    if constexpr (MODE == rtk::kTrace || E > RTK_PAIR_MAX_E) {
+        return fail(RTK_EINVAL, "internal: paired-row kernel not instantiated");
+    } else {
+        // two selection staging buffers per warp
+        const size_t smem = (size_t)(kThreads / 32) * 2 * rtk::LaneRow<E, false>::kStageBytes;
+        const bool wide = (reinterpret_cast<uintptr_t>(a.x) & 31) == 0 && a.ldx % 8 == 0;  // 256-bit loads
+        if (a.m == 32 * E && wide) return launch_rows(rtk::rowtopk_pair_kernel<MODE, E, false, true>, a, s, smem);
+        if (a.m == 32 * E) return launch_rows(rtk::rowtopk_pair_kernel<MODE, E, false, false>, a, s, smem);
+        return launch_rows(rtk::rowtopk_pair_kernel<MODE, E, true, false>, a, s, smem);
+    }
+}
+
+template <int MODE, int E>
+int launch_lane(const rtk::Args& a, cudaStream_t s) {
+    if (pair_eligible<MODE, E>(a)) return launch_pair<MODE, E>(a, s);
+    // Long rows: one register tile fed by a shared-memory ring (rtk_big.cuh).
+    if constexpr (E >= RTK_BIG_MIN_E) {
+        if (a.m == 32 * E) return launch_big<MODE, E, false>(a, s);
+        return launch_big<MODE, E, true>(a, s);
+    }
+    // staging buffer per warp: row copy + 32*E indices (no selection in trace mode)
+    const size_t smem = MODE == rtk::kTrace ? 0 : (size_t)(kThreads / 32) * rtk::LaneRow<E, false>::kStageBytes;
+    const bool wide = (reinterpret_cast<uintptr_t>(a.x) & 31) == 0 && a.ldx % 8 == 0;  // 256-bit loads
+    if (a.m == 32 * E && wide) return launch_row_kernel<MODE, rtk::LaneRow<E, false, true>>(a, s, smem);
+    if (a.m == 32 * E) return launch_row_kernel<MODE, rtk::LaneRow<E, false, false>>(a, s, smem);
+    return launch_row_kernel<MODE, rtk::LaneRow<E, true, false>>(a, s, smem);
+}
+
+template <int MODE>
+int dispatch(const rtk::Args& a, cudaStream_t s) {
+    const int m = a.m;
+    const bool vec4 = (m % 4 == 0) && (a.ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
+#ifdef RTK_TUNE_E  // tuning builds: only one register-tile width (fast to compile)
+    if (m <= 1024 && vec4 && (m + 127) / 128 * 4 == RTK_TUNE_E) return launch_lane<MODE, RTK_TUNE_E>(a, s);
+    return launch_row_kernel<MODE, rtk::GlobalRow>(a, s, 0);
+#else
+    if (m <= 1024 && vec4) {
+        // elements per lane: ceil(m / 32) rounded up to a multiple of 4
+        switch ((m + 127) / 128) {
+            case 1: return launch_lane<MODE, 4>(a, s);
+            case 2: return launch_lane<MODE, 8>(a, s);
+            case 3: return launch_lane<MODE, 12>(a, s);
+            case 4: return launch_lane<MODE, 16>(a, s);
+            case 5: return launch_lane<MODE, 20>(a, s);
+            case 6: return launch_lane<MODE, 24>(a, s);
+            case 7: return launch_lane<MODE, 28>(a, s);
+            default: return launch_lane<MODE, 32>(a, s);
+        }
+    }
+    if (m <= 1024) {
+        const int c = (m + 31) / 32;
+        if (c <= 1) return launch_reg<MODE, 1, 1>(a, s);
+        if (c <= 2) return launch_reg<MODE, 1, 2>(a, s);
+        if (c <= 4) return launch_reg<MODE, 1, 4>(a, s);
+        if (c <= 8) return launch_reg<MODE, 1, 8>(a, s);
+        if (c <= 16) return launch_reg<MODE, 1, 16>(a, s);
+        return launch_reg<MODE, 1, 32>(a, s);
+    }
+    return launch_row_kernel<MODE, rtk::GlobalRow>(a, s, 0);
+#endif
+}
+
+
+}  // namespace rtk_dispatch

@@ -1,0 +1,4 @@
+// rtk_dispatch_trace.cu -- instantiates the trace-mode kernels (see rtk_dispatch.cuh).
+#include "rtk_dispatch.cuh"
+
+int rtk_dispatch_trace(const rtk::Args& a, cudaStream_t s) { return rtk_dispatch::dispatch<rtk::kTrace>(a, s); }

@@ -874,7 +874,7 @@ __device__ __forceinline__ void select_exact(const Row& row, const Args& a, int 
 }
 
 // Rows holding a NaN: record the first offending row (batch.py:37-39).  Cold.
-__device__ __noinline__ void report_nan(unsigned* nan_row, unsigned r, int lane) {
+static __device__ __noinline__ void report_nan(unsigned* nan_row, unsigned r, int lane) {
     if (lane == 0 && nan_row) atomicMin(nan_row, r);
 }
 
@@ -1014,6 +1014,7 @@ __global__ void __launch_bounds__(RTK_CTA_THREADS, RTK_MIN_CTAS) rowtopk_kernel(
     }
 }
 
+#ifdef RTK_DEFINE_FLAT_KERNELS  // defined once, in rtk_capi.cu
 // k == M shortcut (_kernels.py:173-179): copy the row, indices 0..M-1, trace (0, DEGENERATE).
 __global__ void __launch_bounds__(256) full_copy_kernel(Args a) {
     const long long total = a.n * (long long)a.m;
@@ -1075,5 +1076,7 @@ __global__ void __launch_bounds__(256) count_ge_kernel(Args a, const float* __re
         if (lane == 0) counts[r] = c;
     }
 }
+
+#endif  // RTK_DEFINE_FLAT_KERNELS
 
 }  // namespace rtk
