@@ -104,6 +104,20 @@ RTK_API int rtk_row_min_max_f32(const float *x, int64_t n, int64_t m, int64_t ld
 RTK_API int rtk_count_ge_f32(const float *x, int64_t n, int64_t m, int64_t ldx, const float *thres,
                      int32_t *counts, void *stream);
 
+/* MaxK-GNN consumer shapes.  The row top-k output (values,
+ * ascending int32 indices, k per row) is the fixed-k-per-row sparse layout
+ * the MaxK-GNN aggregation consumes; these convert between it and dense rows.
+ * rtk_scatter_rows_f32: out[r, idx[r,j]] = vals[r,j], 0 elsewhere (out is
+ *   n x m with row stride ldo >= m; vals/idx share row stride ldv >= k);
+ *   the MaxK nonlinearity's dense output, and the backward of the gather.
+ * rtk_gather_rows_f32: vals[r,j] = dense[r, idx[r,j]] (dense row stride
+ *   ldd >= m); the backward of the MaxK nonlinearity.
+ * Indices outside [0, m) are skipped (scatter) / read as 0 (gather). */
+RTK_API int rtk_scatter_rows_f32(const float *vals, const int32_t *idx, int64_t ldv, int64_t n, int32_t k,
+                         int64_t m, float *out, int64_t ldo, void *stream);
+RTK_API int rtk_gather_rows_f32(const float *dense, int64_t ldd, const int32_t *idx, int64_t ldv, int64_t n,
+                        int32_t k, int64_t m, float *vals, void *stream);
+
 /* File-level job: RTKM matrix file -> row top-k on the current CUDA device
  * -> RTKR result file, streamed in chunks of `chunk_rows` rows (0 = ~64 MB):
  * pread into pinned host buffers, H2D, kernel, D2H and pwrite of consecutive

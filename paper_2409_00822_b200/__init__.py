@@ -32,6 +32,7 @@ from .errors import (  # noqa: F401
     VerificationError,
 )
 from .io import load_matrix, load_result, save_matrix, save_result, topk_file  # noqa: F401
+from .maxk import gather_rows, maxk, maxk_dense, scatter_rows, to_sparse_csr  # noqa: F401
 from .select import (  # noqa: F401
     DEFAULT_HARD_CAP,
     DEFAULT_MAX_ITER,
@@ -54,5 +55,5 @@ __all__ = [
     "REGISTER_COLS_LIMIT", "RowTopKError", "SOFT_COLS_LIMIT", "SearchConfig", "SearchMode", "SearchTrace",
     "TopKResult", "as_matrix", "as_row", "batch_topk", "chunk_ranges", "count_ge", "early_stop_topk",
     "exact_topk", "exact_trace", "min_max", "oracle_topk", "resolve_workers", "load_matrix", "load_result",
-    "save_matrix", "save_result", "topk_file",
+    "save_matrix", "save_result", "topk_file", "maxk", "maxk_dense", "scatter_rows", "gather_rows", "to_sparse_csr",
 ]

@@ -35,6 +35,8 @@ SIGNATURES = {
     "rtk_count_ge_f32": (ctypes.c_int, [_p, _i64, _i64, _i64, _p, _p, _p]),
     "rtk_topk_file_f32": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, _i32, _i32, ctypes.c_double, _i32, _i32,
                                          _i64, _p]),
+    "rtk_scatter_rows_f32": (ctypes.c_int, [_p, _p, _i64, _i64, _i32, _i64, _p, _i64, _p]),
+    "rtk_gather_rows_f32": (ctypes.c_int, [_p, _i64, _p, _i64, _i64, _i32, _i64, _p, _p]),
     "rtk_last_error": (ctypes.c_char_p, []),
     "rtk_version": (ctypes.c_int, []),
     "rtk_launch_shape": (ctypes.c_int, [_i64, _i32, _i32, _p, _p, _p]),

@@ -1,0 +1,89 @@
+"""MaxK-GNN consumer shapes: scatter / gather kernels against
+torch's scatter_/gather on the same indices, the autograd ops against a plain
+PyTorch formulation of MaxK, and the CSR view against the dense form."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2409_00822_b200 as rtk  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2409_00822_b200 import _build
+
+    _build.build()
+    torch.cuda.set_device(0)
+
+
+@pytest.mark.parametrize("n,m,k", [(1, 1, 1), (7, 5, 3), (1000, 256, 32), (333, 97, 11), (64, 1500, 128),
+                                   (4099, 2048, 64), (10, 4096, 4096)])
+def test_scatter_gather_match_torch(n, m, k):
+    g = torch.Generator(device="cuda").manual_seed(n * 7 + m)
+    x = torch.randn(n, m, device="cuda", generator=g)
+    res = rtk.batch_topk(x, rtk.BatchConfig(k=k))
+    dense = rtk.scatter_rows(res.values, res.indices, m)
+    want = torch.zeros(n, m, device="cuda").scatter_(1, res.indices.long(), res.values)
+    assert torch.equal(dense, want)
+    back = rtk.gather_rows(dense, res.indices)
+    assert torch.equal(back, torch.gather(dense, 1, res.indices.long()))
+    assert torch.equal(back, res.values)
+
+
+def test_scatter_strided_and_unaligned_rows():
+    x = torch.randn(300, 130, device="cuda")
+    res = rtk.batch_topk(x, rtk.BatchConfig(k=9))
+    dense = rtk.scatter_rows(res.values, res.indices, 130)  # m % 4 != 0: scalar stores
+    assert torch.equal(dense, torch.zeros(300, 130, device="cuda").scatter_(1, res.indices.long(), res.values))
+    big = torch.randn(300, 200, device="cuda")
+    view = big[:, 3:133]  # gather from a strided, unaligned view
+    assert torch.equal(rtk.gather_rows(view, res.indices), torch.gather(view, 1, res.indices.long()))
+
+
+def _torch_maxk_dense(x, k):
+    """Plain PyTorch MaxK (reference formulation): keep the top-k per row."""
+    v, i = torch.topk(x, k, dim=1)
+    return torch.zeros_like(x).scatter(1, i, v)
+
+
+@pytest.mark.parametrize("search", [rtk.SearchConfig.exact(), rtk.SearchConfig.early_stop(4)])
+def test_maxk_autograd(search):
+    n, m, k = 2048, 256, 32
+    x = torch.randn(n, m, device="cuda", requires_grad=True)
+    vals, idx = rtk.maxk(x, k, search)
+    want = rtk.batch_topk(x.detach(), rtk.BatchConfig(k=k, search=search))
+    assert torch.equal(vals, want.values) and torch.equal(idx, want.indices)
+    gv = torch.randn_like(vals)
+    (vals * gv).sum().backward()
+    expect = torch.zeros(n, m, device="cuda").scatter_(1, idx.long(), gv)
+    assert torch.equal(x.grad, expect)
+
+
+def test_maxk_dense_matches_torch_formulation():
+    n, m, k = 1024, 256, 32
+    x = torch.randn(n, m, device="cuda", dtype=torch.float32)
+    x1 = x.clone().requires_grad_(True)
+    x2 = x.clone().requires_grad_(True)
+    y1 = rtk.maxk_dense(x1, k)
+    y2 = _torch_maxk_dense(x2, k)  # exact mode = the true top-k on distinct N(0,1) values
+    assert torch.equal(y1, y2)
+    g = torch.randn(n, m, device="cuda")
+    (y1 * g).sum().backward()
+    (y2 * g).sum().backward()
+    assert torch.equal(x1.grad, x2.grad)
+
+
+def test_sparse_csr_view_spmm():
+    n, m, k = 500, 256, 32
+    x = torch.randn(n, m, device="cuda")
+    vals, idx = rtk.maxk(x, k)
+    csr = rtk.to_sparse_csr(vals, idx, m)
+    dense = rtk.scatter_rows(vals, idx, m)
+    assert torch.equal(csr.to_dense(), dense)
+    w = torch.randn(m, 64, device="cuda")
+    assert torch.allclose(torch.sparse.mm(csr, w), dense @ w, rtol=1e-4, atol=1e-4)
