@@ -24,4 +24,9 @@ run_full m1024_exact exact 1048576:1024:64
 run_full m1024_early early 1048576:1024:64
 run_full m512_early early 1048576:512:64
 timeout 900 python tools/sweep_bench.py --out $OUT/sweep.json > $OUT/sweep.log 2>&1
+timeout 600 python tools/maxk_bench.py > $OUT/maxk_bench.json 2> $OUT/maxk_bench.err
+timeout 600 python tools/file_bench.py /dev/shm > $OUT/file_bench_tmpfs.json 2> $OUT/file_bench.err
+timeout 300 python tools/pcie_probe.py > $OUT/pcie_probe.json 2>&1
+timeout 900 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
 echo done > $OUT/DONE
