@@ -58,12 +58,14 @@ __global__ void __launch_bounds__(RTK_BIG_THREADS, BigMinCtas<E, MASKED>::value)
     unsigned slot = 0;
     Row row;
     for (;;) {
-        cp_async_wait<D - 1>();  // this row's group has landed
+        cp_async_wait<D - 1>();  // this lane's copies of this row have landed ...
+        __syncwarp();            // ... and (chunks go to their owner lanes) every lane's
         const unsigned sl = ring + slot * Row::kRowBytes;
         row.load_smem(sl, a.m, lane);
         const unsigned long long rpre = (unsigned long long)r + (unsigned long long)D * nw;
         // refill after the tile has been read (the token orders the LDGSTS after the LDS)
         process_row<MODE, TRACES>(row, r, a, lane, sbase, fp, [&](unsigned tok) {
+            __syncwarp();  // every lane has read its tile out of the slot before any refill lands
             if (rpre < n) Row::stage_async(row_ptr(a.x, (unsigned)rpre + (tok & a.opaque_zero), ldx_b), a.m, lane, sl);
             cp_async_commit();
         });

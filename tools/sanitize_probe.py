@@ -1,0 +1,50 @@
+"""Small launches of every kernel family under compute-sanitizer: paired-row
+(E=4, 8; masked/unmasked; odd N), long-row (E=12..32), general kernels
+(traces, RegRow, GlobalRow), k == M, NaN rows, the host pipeline, the file
+job and the MaxK scatter/gather.  Exits non-zero on a parity mismatch."""
+import os
+import sys
+import tempfile
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import oracle  # noqa: E402
+import paper_2409_00822_b200 as rtk  # noqa: E402
+
+
+def main():
+    rng = np.random.default_rng(0)
+    for m in (4, 8, 100, 128, 256, 257, 384, 512, 777, 1024, 1500):
+        n = 67
+        x = rng.standard_normal((n, m), dtype=np.float32)
+        x[5] = 1.0
+        x[9, : m // 2] = np.inf
+        for k in sorted({1, min(33, m), m}):
+            for search, mode, mi in ((rtk.SearchConfig.exact(), "exact", 4), (rtk.SearchConfig.early_stop(3), "early", 3)):
+                v, i, t, r = oracle.ref_batch(x, k, mode, max_iter=mi)
+                for traces in (False, True):
+                    res = rtk.batch_topk(torch.from_numpy(x).cuda(), rtk.BatchConfig(k=k, search=search, collect_traces=traces))
+                    assert np.array_equal(res.indices.cpu().numpy(), i), (m, k, mode, traces)
+                    assert np.array_equal(res.values.cpu().numpy().view(np.uint32), v.view(np.uint32)), (m, k, mode)
+        xn = x.copy()
+        xn[40, m - 1] = np.nan
+        try:
+            rtk.batch_topk(xn, rtk.BatchConfig(k=1))
+            raise AssertionError("NaN not reported")
+        except rtk.NaNInputError:
+            pass
+    xd = torch.randn(1000, 256, device="cuda")
+    res = rtk.batch_topk(xd, rtk.BatchConfig(k=32))
+    d = rtk.scatter_rows(res.values, res.indices, 256)
+    assert torch.equal(rtk.gather_rows(d, res.indices), res.values)
+    with tempfile.TemporaryDirectory() as tdir:
+        p, q = os.path.join(tdir, "x.rtkm"), os.path.join(tdir, "o.rtkr")
+        rtk.save_matrix(rng.standard_normal((3000, 96), dtype=np.float32), p)
+        rtk.topk_file(p, q, rtk.BatchConfig(k=7), chunk_rows=1000)
+    print("sanitize probe ok")
+
+
+if __name__ == "__main__":
+    main()
