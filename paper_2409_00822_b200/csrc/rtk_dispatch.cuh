@@ -13,6 +13,7 @@
 #include "rtk_big.cuh"
 #include "rtk_kernels.cuh"
 #include "rtk_pair.cuh"
+#include "rtk_block.cuh"
 
 // library-internal (rtk_capi.cu)
 int rtk_fail(int code, const char* fmt, ...);
@@ -138,11 +139,46 @@ int launch_lane(const rtk::Args& a, cudaStream_t s) {
     return launch_row_kernel<MODE, rtk::LaneRow<E, true, false>>(a, s, smem);
 }
 
+// Long rows (rtk_block.cuh): one CTA of W warps per row, 1024 < M <= 8192.
+template <int MODE, int W, bool TRACES>
+int launch_block_kernel(const rtk::Args& a, cudaStream_t s) {
+    using Tile = rtk::LaneRow<32, true, false>;
+    const int threads = W * 32;
+    const size_t smem = (((size_t)8 * a.k + 15) & ~(size_t)15) + (size_t)W * Tile::kRowBytes;
+    auto kernel = rtk::rowtopk_block_kernel<MODE, W, TRACES>;
+    long long grid = (long long)rtk_device_sms() * rtk_ctas_per_sm(reinterpret_cast<const void*>(kernel), smem, threads);
+    if (grid > a.n) grid = a.n;
+    if (grid < 1) grid = 1;
+    kernel<<<(unsigned)grid, threads, smem, s>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(RTK_ECUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+    return RTK_OK;
+}
+
+template <int MODE, int W>
+int launch_block(const rtk::Args& a, cudaStream_t s) {
+    if constexpr (MODE == rtk::kTrace) {
+        return launch_block_kernel<MODE, W, true>(a, s);
+    } else {
+        if ((a.iters != nullptr) != (a.reasons != nullptr))
+            return fail(RTK_EINVAL, "iters and reasons must be both NULL or both non-NULL");
+        if (a.iters != nullptr) return launch_block_kernel<MODE, W, true>(a, s);
+        return launch_block_kernel<MODE, W, false>(a, s);
+    }
+}
+
 template <int MODE>
 int dispatch(const rtk::Args& a, cudaStream_t s) {
     const int m = a.m;
     const bool vec4 = (m % 4 == 0) && (a.ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
-#ifdef RTK_TUNE_E  // tuning builds: only one register-tile width (fast to compile)
+#ifdef RTK_TUNE_BLOCK  // tuning builds: only the CTA-per-row kernels (M > 1024)
+    if (m > 1024 && m <= 8192 && vec4) {
+        if (m <= 2048) return launch_block<MODE, 2>(a, s);
+        if (m <= 4096) return launch_block<MODE, 4>(a, s);
+        return launch_block<MODE, 8>(a, s);
+    }
+    return launch_row_kernel<MODE, rtk::GlobalRow>(a, s, 0);
+#elif defined(RTK_TUNE_E)  // tuning builds: only one register-tile width (fast to compile)
     if (m <= 1024 && vec4 && (m + 127) / 128 * 4 == RTK_TUNE_E) return launch_lane<MODE, RTK_TUNE_E>(a, s);
     return launch_row_kernel<MODE, rtk::GlobalRow>(a, s, 0);
 #else
@@ -167,6 +203,11 @@ int dispatch(const rtk::Args& a, cudaStream_t s) {
         if (c <= 8) return launch_reg<MODE, 1, 8>(a, s);
         if (c <= 16) return launch_reg<MODE, 1, 16>(a, s);
         return launch_reg<MODE, 1, 32>(a, s);
+    }
+    if (m <= 8192 && vec4) {
+        if (m <= 2048) return launch_block<MODE, 2>(a, s);
+        if (m <= 4096) return launch_block<MODE, 4>(a, s);
+        return launch_block<MODE, 8>(a, s);
     }
     return launch_row_kernel<MODE, rtk::GlobalRow>(a, s, 0);
 #endif

@@ -176,6 +176,7 @@ __device__ __forceinline__ unsigned warp_incl_scan(unsigned x) {
 template <int V, int C, bool MASKED>
 struct RegRow {
     static constexpr bool kStaged = true;  // selection goes through shared memory
+    static constexpr bool kBlock = false;  // one warp per row
     static constexpr int kPad = 0;         // staging holds exactly k entries
     __host__ __device__ static constexpr unsigned stage_bytes(int k) { return (8u * (unsigned)k + 15u) & ~15u; }
     static constexpr int kV = V;
@@ -355,6 +356,7 @@ __device__ __forceinline__ void flush_row(unsigned sbase, int k, float* __restri
 template <int E, bool MASKED, bool WIDE = false>
 struct LaneRow {
     static constexpr bool kStaged = true;
+    static constexpr bool kBlock = false;
     static constexpr int kSlots = E;
     static constexpr int kPad = 32 * E;  // staging entries per warp
     float v[E];
@@ -624,6 +626,7 @@ struct LaneRowCut : LaneRow<E, MASKED, false> {
 // chunk count, every pass re-reading the row (L1/L2 resident after pass 1).
 struct GlobalRow {
     static constexpr bool kStaged = false;  // selection stores straight to global
+    static constexpr bool kBlock = false;
     static constexpr int kPad = 0;
     __host__ __device__ static constexpr unsigned stage_bytes(int) { return 0u; }
     const float* __restrict__ p;
@@ -701,6 +704,24 @@ struct GlobalRow {
 
 // ---------------------------------------------------------- the searches
 
+// Row-level reductions: one warp per row (warp collectives) or a CTA per
+// row (Row::kBlock, rtk_block.cuh: warp collectives + a shared-memory
+// combine; every thread of the CTA gets the row's value).
+template <class Row>
+__device__ __forceinline__ int row_count(const Row& row, int lane_biased) {
+    if constexpr (Row::kBlock)
+        return row.count(lane_biased);
+    else
+        return warp_count(lane_biased);
+}
+template <class Row>
+__device__ __forceinline__ bool row_leader(int lane) {
+    if constexpr (Row::kBlock)
+        return threadIdx.x == 0;
+    else
+        return lane == 0;
+}
+
 // Algorithm 1 loop (_kernels.py:64-84), entered only when the loop-head test
 // passed at it == 0.  FP: eps_rel == 0 and mx0 finite, so the float64 head
 // test `mx - mn > eps` is the fp32 `mx > mn`; it is evaluated at the end of
@@ -723,7 +744,7 @@ __device__ __forceinline__ int exact_loop(const Row& row, int kb, double eps, in
             mid = mid_fast(mn, mx);
             inside = (mn < mid) && (mid < mx);
             lane_last = row.lane_count_ge(mid);
-            cnt = warp_count(lane_last);
+            cnt = row_count(row, lane_last);
             const bool lt = cnt < kb;
             eq = cnt == kb;
             mx = lt ? mid : mx;
@@ -741,7 +762,7 @@ __device__ __forceinline__ int exact_loop(const Row& row, int kb, double eps, in
             ++it;
             mid = SAFE ? mid_fast(mn, mx) : mid_exact(mn, mx);
             lane_last = row.lane_count_ge(mid);
-            cnt = warp_count(lane_last);
+            cnt = row_count(row, lane_last);
             const bool lt = cnt < kb;
             eq = cnt == kb;
             stuck = mid == (lt ? mx : mn);
@@ -785,7 +806,7 @@ __device__ __forceinline__ bool exact_loop_fast(const Row& row, int kb, int step
         ++it;
         mid = mid_fast(mn, mx);
         lc = row.lane_count_ge(mid);
-        c = warp_count(lc);
+        c = row_count(row, lc);
         const bool lt = c < kb;
         mx = lt ? mid : mx;
         mn = lt ? mn : mid;
@@ -808,7 +829,7 @@ __device__ __forceinline__ void early_loop(const Row& row, int kb, int max_iter,
     for (int i = 0; i < max_iter; ++i) {
         const float mid = SAFE ? mid_fast(mn, mx) : mid_exact(mn, mx);
         const int lc = row.lane_count_ge(mid);
-        const bool lt = warp_count(lc) < kb;
+        const bool lt = row_count(row, lc) < kb;
         mx = lt ? mid : mx;
         mn = lt ? mn : mid;
         lane_mn = lt ? lane_mn : lc;
@@ -822,7 +843,9 @@ __device__ __forceinline__ void early_loop(const Row& row, int kb, int max_iter,
 template <class Row>
 __device__ __forceinline__ void flush_staged(unsigned sbase, int k, float* __restrict__ ov, int* __restrict__ oi,
                                              int lane, unsigned dep = 0u) {
-    if constexpr (Row::kPad > 0)
+    if constexpr (Row::kBlock)
+        Row::flush_block(sbase + dep, k, ov, oi);
+    else if constexpr (Row::kPad > 0)
         Row::flush(sbase + dep, k, ov, oi, lane);
     else
         flush_row(sbase + dep, k, ov, oi, lane);
@@ -856,7 +879,7 @@ __device__ __forceinline__ void select_exact(const Row& row, const Args& a, int 
     if (use_mx) {
         t = mx;
         lane_t = row.lane_count_ge(mx);
-        ca = warp_count(lane_t) - kCountBias;
+        ca = row_count(row, lane_t) - kCountBias;
     }
     if constexpr (Row::kStaged) {
         unsigned sink = 0;
@@ -946,7 +969,7 @@ __device__ __forceinline__ void row_body(const Row& row, unsigned r, const Args&
         if constexpr (MODE == kExact) select_exact(row, a, lane, sbase, fp, reason, thres, mn, mx, cnt, lane_t, ov, oi);
     }
     if constexpr (TRACES) {
-        if (lane == 0) {
+        if (row_leader<Row>(lane)) {
             a.iters[r] = it;
             a.reasons[r] = (signed char)reason;
         }
@@ -963,8 +986,14 @@ __device__ __forceinline__ void process_row(const Row& row, unsigned r, const Ar
     float mnl, mxl;
     row.lane_min_max(a.m, lane, mnl, mxl);
     after_load(__float_as_uint(mnl) ^ __float_as_uint(mxl));
-    const float mn0 = warp_min_nan(mnl), mx0 = warp_max(mxl);
-    if (mn0 != mn0) report_nan(a.nan_row, r, lane);
+    float mn0, mx0;
+    if constexpr (Row::kBlock) {
+        row.reduce_min_max(mnl, mxl, mn0, mx0);
+    } else {
+        mn0 = warp_min_nan(mnl);
+        mx0 = warp_max(mxl);
+    }
+    if (mn0 != mn0 && row_leader<Row>(lane)) report_nan(a.nan_row, r, 0);
     row_body<MODE, TRACES>(row, r, a, lane, sbase, fp, mn0, mx0);
 }
 

@@ -167,14 +167,15 @@ def _mixed_rows(rng, n, m):
     return np.stack(rows)
 
 
-@pytest.mark.parametrize("m", [4, 8, 100, 128, 200, 256, 260, 384, 500, 512, 640, 768, 1000, 1024])
+@pytest.mark.parametrize("m", [4, 8, 100, 128, 200, 256, 260, 384, 500, 512, 640, 768, 1000, 1024, 1028, 2048, 3000,
+                               4096, 8192])
 def test_fast_paths_mixed_rows_vs_oracle(oracle_lib, m):
     """The no-trace hot paths (paired-row kernel for M <= 256, long-row kernel
     above, masked and unmasked tiles) on odd row counts mixing fast-loop rows
     with rows that need the general per-row path, vs the oracle; then the
     trace path on the same input."""
     rng = np.random.default_rng(1000 + m)
-    n = 777 if m <= 256 else 333
+    n = 777 if m <= 256 else (333 if m <= 1024 else 61)
     x = _mixed_rows(rng, n, m)
     ks = sorted({1, min(7, m), min(32, m), max(1, m // 3), max(1, m - 1)})
     searches = [("exact", 4, 0.0, 64), ("exact", 4, 0.0, 7), ("exact", 4, 1e-4, 64), ("early", 2, 0.0, 64),
@@ -197,7 +198,7 @@ def test_fast_paths_many_grid_steps_vs_oracle(oracle_lib):
     the oracle."""
     g = torch.Generator(device="cuda").manual_seed(11)
     for n, m, k in ((300_001, 256, 32), (300_001, 128, 16), (120_001, 1024, 64), (150_001, 512, 64),
-                    (100_003, 768, 128)):
+                    (100_003, 768, 128), (20_001, 2048, 64), (9_001, 8192, 256)):
         x = torch.randn(n, m, device="cuda", generator=g)
         rows = torch.tensor([0, 1, 2, 3, n // 3, n // 2 + 1, n - 4, n - 3, n - 2, n - 1], device="cuda")
         xs = x[rows].cpu().numpy()
