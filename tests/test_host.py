@@ -129,3 +129,29 @@ def test_product_package_never_imports_the_oracle():
                     src = f.read()
                 assert not re.search(r"^\s*(import|from)\s+oracle\b", src, re.M), fn
                 assert "rtk_oracle" not in src and "librtk_oracle" not in src, fn
+
+
+def test_file_job_rejects_bad_files_before_touching_the_gpu(lib, tmp_path):
+    """rtk_topk_file_f32 validates the RTKM header (io.py:32-43 order) before
+    any CUDA call, so these paths run on a CPU box."""
+    import struct
+
+    dims = (ctypes.c_int64 * 3)()
+    out = str(tmp_path / "o.rtkr").encode()
+    rc = lib.rtk_topk_file_f32(str(tmp_path / "missing.rtkm").encode(), out, 1, 0, 0.0, 64, 4, 0, dims)
+    assert rc == _native.RTK_EIO
+    bad = tmp_path / "bad.rtkm"
+    bad.write_bytes(b"NOPE" + b"\x00" * 40)
+    assert lib.rtk_topk_file_f32(str(bad).encode(), out, 1, 0, 0.0, 64, 4, 0, dims) == _native.RTK_EFORMAT
+    assert b"expected magic b'RTKM'" in lib.rtk_last_error()
+    v2 = tmp_path / "v2.rtkm"
+    v2.write_bytes(struct.pack("<4sIQQ", b"RTKM", 2, 1, 1) + b"\x00" * 4)
+    assert lib.rtk_topk_file_f32(str(v2).encode(), out, 1, 0, 0.0, 64, 4, 0, dims) == _native.RTK_EFORMAT
+    tr = tmp_path / "tr.rtkm"
+    tr.write_bytes(struct.pack("<4sIQQ", b"RTKM", 1, 4, 4) + b"\x00" * 20)
+    assert lib.rtk_topk_file_f32(str(tr).encode(), out, 1, 0, 0.0, 64, 4, 0, dims) == _native.RTK_ETRUNC
+    assert (dims[0], dims[1]) == (4, 4)
+    short = tmp_path / "short.rtkm"
+    short.write_bytes(b"RTKM\x01")
+    assert lib.rtk_topk_file_f32(str(short).encode(), out, 1, 0, 0.0, 64, 4, 0, dims) == _native.RTK_ETRUNC
+    assert lib.rtk_topk_file_f32(str(tr).encode(), out, 1, 7, 0.0, 64, 4, 0, dims) == _native.RTK_EINVAL
