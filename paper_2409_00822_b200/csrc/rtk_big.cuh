@@ -77,3 +77,102 @@ __global__ void __launch_bounds__(RTK_BIG_THREADS, BigMinCtas<E, MASKED>::value)
 }
 
 }  // namespace rtk
+
+// ---------------------------------------------------------------------------
+// TMA variant (unmasked rows, E = 16 or 32): one elected lane per warp loads
+// the whole next row into the warp's slot with a tensor-map bulk copy
+// (cp.async.bulk.tensor, completion on an mbarrier), the tensor map views the
+// matrix as [n][32][E] floats and applies the hardware swizzle that makes the
+// lane-contiguous LDS.128 reads conflict-free without padding (128B swizzle:
+// 16-byte chunk c of lane l sits at c ^ (l & 7); 64B: c ^ ((l >> 1) & 3)).
+#include <cuda.h>
+
+namespace rtk {
+
+template <int E>
+struct TmaRow : LaneRowCut<E, false> {
+    static_assert(E == 16 || E == 32, "TMA rows: E = 16 (64B swizzle) or 32 (128B swizzle)");
+    static constexpr unsigned kSlotBytes = 32u * E * 4u;   // raw row, swizzled in place
+    static constexpr unsigned kSlotAlign = E == 32 ? 1024u : 512u;
+    __device__ __forceinline__ static unsigned phys_chunk(int l, int c) {
+        return E == 32 ? (unsigned)(c ^ (l & 7)) : (unsigned)(c ^ ((l >> 1) & 3));
+    }
+    __device__ __forceinline__ void load_swizzled(unsigned slot, int lane) {
+        const unsigned base = slot + (unsigned)lane * E * 4u;
+#pragma unroll
+        for (int c = 0; c < E / 4; ++c) {
+            const float4 q = lds128(base + 16u * phys_chunk(lane, c));
+            this->v[4 * c] = q.x;
+            this->v[4 * c + 1] = q.y;
+            this->v[4 * c + 2] = q.z;
+            this->v[4 * c + 3] = q.w;
+        }
+    }
+};
+
+__device__ __forceinline__ void mbar_init(unsigned bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tma_row(unsigned slot, const CUtensorMap* map, int row, unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(slot),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(0), "r"(0), "r"(row), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned phase) {
+    unsigned done = 0;
+    do {
+        asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p;}"
+                     : "=r"(done)
+                     : "r"(bar), "r"(phase)
+                     : "memory");
+    } while (!done);
+}
+
+template <int MODE, int E, bool TRACES>
+__global__ void __launch_bounds__(RTK_BIG_THREADS, BigMinCtas<E, false>::value)
+    rowtopk_big_tma_kernel(Args a, const __grid_constant__ CUtensorMap map) {
+    using Row = TmaRow<E>;
+    extern __shared__ __align__(1024) float smem[];
+    const int lane = threadIdx.x & 31;
+    const int wid = __shfl_sync(kFull, (int)(threadIdx.x >> 5), 0);
+    const unsigned wpc = blockDim.x >> 5;
+    const unsigned base = (unsigned)__cvta_generic_to_shared(smem);
+    const unsigned stage_bytes = Row::stage_bytes(a.k);
+    const unsigned slots = (base + wpc * stage_bytes + Row::kSlotAlign - 1) & ~(Row::kSlotAlign - 1);
+    const unsigned slot = slots + (unsigned)wid * Row::kSlotBytes;
+    const unsigned bar = slots + wpc * Row::kSlotBytes + 8u * (unsigned)wid;
+    const unsigned sbase = base + (unsigned)wid * stage_bytes;
+    const unsigned nw = gridDim.x * wpc;
+    const unsigned long long n = (unsigned long long)a.n;
+    unsigned r = blockIdx.x * wpc + (unsigned)wid;
+    if (r >= n) return;
+    const bool fp = a.eps_rel == 0.0;
+    if (lane == 0) {
+        mbar_init(bar);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        tma_row(slot, &map, (int)r, bar, Row::kSlotBytes);
+    }
+    __syncwarp();
+    unsigned phase = 0;
+    Row row;
+    for (;;) {
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        row.load_swizzled(slot, lane);
+        const unsigned long long rn = (unsigned long long)r + nw;
+        process_row<MODE, TRACES>(row, r, a, lane, sbase, fp, [&](unsigned tok) {
+            __syncwarp();  // every lane has read the slot
+            if (lane == 0 && rn < n) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                tma_row(slot, &map, (int)(rn + (tok & a.opaque_zero)), bar, Row::kSlotBytes);
+            }
+        });
+        if (rn >= n) break;
+        r = (unsigned)rn;
+    }
+}
+
+}  // namespace rtk

@@ -5,6 +5,7 @@
 // instantiation (cached per device), and launch on the caller's stream.  No
 // allocation, no synchronisation.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <map>
 #include <tuple>
@@ -168,6 +169,31 @@ int rowtopk_common(int mode, const float* x, int64_t n, int64_t m, int64_t ldx, 
 }  // namespace
 
 int rtk_device_sms() { return device_sms(); }
+
+// Tensor map of x viewed as [n][32][e] floats (row stride ldx), box = one row,
+// swizzle matching the row width (128B for e = 32, 64B for e = 16).  The
+// driver entry point is fetched once through the runtime (no -lcuda).
+bool rtk_encode_row_map(CUtensorMap* map, const float* x, long long n, int e, long long ldx) {
+    static std::once_flag once;
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    std::call_once(once, [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    });
+    if (!encode || (reinterpret_cast<uintptr_t>(x) & 15) || (ldx * 4) % 16) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)e, 32, (cuuint64_t)n};
+    const cuuint64_t strides[2] = {(cuuint64_t)e * 4, (cuuint64_t)ldx * 4};
+    const cuuint32_t box[3] = {(cuuint32_t)e, 32, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(x), dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              e == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
 int rtk_ctas_per_sm(const void* kernel, size_t smem, int threads) { return ctas_per_sm(kernel, smem, threads); }
 
 extern "C" {

@@ -22,6 +22,7 @@ int rtk_ctas_per_sm(const void* kernel, size_t smem, int threads);
 int rtk_dispatch_exact(const rtk::Args& a, cudaStream_t s);
 int rtk_dispatch_early(const rtk::Args& a, cudaStream_t s);
 int rtk_dispatch_trace(const rtk::Args& a, cudaStream_t s);
+bool rtk_encode_row_map(CUtensorMap* map, const float* x, long long n, int e, long long ldx);
 
 namespace rtk_dispatch {
 
@@ -84,8 +85,42 @@ int launch_big_kernel(const rtk::Args& a, cudaStream_t s) {
     return launch_rows(rtk::rowtopk_big_kernel<MODE, E, MASKED, TRACES>, a, s, smem, RTK_BIG_THREADS);
 }
 
+// TMA staging for unmasked long rows with E = 16 / 32 (rtk_big.cuh).
+#ifndef RTK_USE_TMA
+#define RTK_USE_TMA 1
+#endif
+template <int MODE, int E, bool TRACES>
+int launch_big_tma_kernel(const rtk::Args& a, cudaStream_t s, const CUtensorMap& map) {
+    using Row = rtk::TmaRow<E>;
+    constexpr int wpc = RTK_BIG_THREADS / 32;
+    const size_t smem = (size_t)wpc * Row::stage_bytes(a.k) + Row::kSlotAlign + (size_t)wpc * (Row::kSlotBytes + 8);
+    auto kernel = rtk::rowtopk_big_tma_kernel<MODE, E, TRACES>;
+    const long long blocks_needed = (a.n + wpc - 1) / wpc;
+    long long grid = (long long)rtk_device_sms() * rtk_ctas_per_sm(reinterpret_cast<const void*>(kernel), smem,
+                                                                   RTK_BIG_THREADS);
+    if (grid > blocks_needed) grid = blocks_needed;
+    if (grid < 1) grid = 1;
+    kernel<<<(unsigned)grid, RTK_BIG_THREADS, smem, s>>>(a, map);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(RTK_ECUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+    return RTK_OK;
+}
+
 template <int MODE, int E, bool MASKED>
 int launch_big(const rtk::Args& a, cudaStream_t s) {
+    if constexpr (RTK_USE_TMA && !MASKED && (E == 16 || E == 32)) {
+        CUtensorMap map;
+        if (a.n < (1LL << 31) && rtk_encode_row_map(&map, a.x, a.n, E, a.ldx)) {
+            if constexpr (MODE == rtk::kTrace) {
+                return launch_big_tma_kernel<MODE, E, true>(a, s, map);
+            } else {
+                if ((a.iters != nullptr) != (a.reasons != nullptr))
+                    return fail(RTK_EINVAL, "iters and reasons must be both NULL or both non-NULL");
+                if (a.iters != nullptr) return launch_big_tma_kernel<MODE, E, true>(a, s, map);
+                return launch_big_tma_kernel<MODE, E, false>(a, s, map);
+            }
+        }
+    }
     if constexpr (MODE == rtk::kTrace) {
         return launch_big_kernel<MODE, E, MASKED, true>(a, s);
     } else {
