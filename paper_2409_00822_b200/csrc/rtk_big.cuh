@@ -135,7 +135,7 @@ template <int MODE, int E, bool TRACES>
 __global__ void __launch_bounds__(RTK_BIG_THREADS, BigMinCtas<E, false>::value)
     rowtopk_big_tma_kernel(Args a, const __grid_constant__ CUtensorMap map) {
     using Row = TmaRow<E>;
-    extern __shared__ __align__(1024) float smem[];
+    extern __shared__ __align__(16) float smem[];  // slots are aligned by hand (kSlotAlign)
     const int lane = threadIdx.x & 31;
     const int wid = __shfl_sync(kFull, (int)(threadIdx.x >> 5), 0);
     const unsigned wpc = blockDim.x >> 5;

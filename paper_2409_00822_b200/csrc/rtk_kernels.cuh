@@ -993,7 +993,9 @@ __device__ __forceinline__ void process_row(const Row& row, unsigned r, const Ar
         mn0 = warp_min_nan(mnl);
         mx0 = warp_max(mxl);
     }
-    if (mn0 != mn0 && row_leader<Row>(lane)) report_nan(a.nan_row, r, 0);
+    // keep the (noinline) call warp-uniform: a divergent call site makes ptxas
+    // guard every later collective with WARPSYNC / ENDCOLLECTIVE
+    if (mn0 != mn0) report_nan(a.nan_row, r, row_leader<Row>(lane) ? 0 : 1);
     row_body<MODE, TRACES>(row, r, a, lane, sbase, fp, mn0, mx0);
 }
 

@@ -26,7 +26,6 @@ namespace {
 
 constexpr int kWarps = 8;        // warps per CTA
 constexpr int kTile = 1024;      // dense columns staged per warp
-constexpr unsigned kFull = 0xffffffffu;
 
 __global__ void __launch_bounds__(kWarps * 32) scatter_rows_kernel(const float* __restrict__ vals,
                                                                    const int32_t* __restrict__ idx, int64_t ldv,
