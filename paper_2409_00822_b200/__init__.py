@@ -18,6 +18,7 @@ from .batch import (  # noqa: F401
     chunk_ranges,
     exact_trace,
     resolve_workers,
+    topk_device,
 )
 from .errors import (  # noqa: F401
     BadMagicError,
@@ -55,5 +56,5 @@ __all__ = [
     "REGISTER_COLS_LIMIT", "RowTopKError", "SOFT_COLS_LIMIT", "SearchConfig", "SearchMode", "SearchTrace",
     "TopKResult", "as_matrix", "as_row", "batch_topk", "chunk_ranges", "count_ge", "early_stop_topk",
     "exact_topk", "exact_trace", "min_max", "oracle_topk", "resolve_workers", "load_matrix", "load_result",
-    "save_matrix", "save_result", "topk_file", "maxk", "maxk_dense", "scatter_rows", "gather_rows", "to_sparse_csr",
+    "save_matrix", "save_result", "topk_file", "topk_device", "maxk", "maxk_dense", "scatter_rows", "gather_rows", "to_sparse_csr",
 ]

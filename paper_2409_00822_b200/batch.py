@@ -407,6 +407,26 @@ def batch_topk(matrix, cfg: BatchConfig) -> BatchResult:
     return BatchResult(vals, idx)
 
 
+def topk_device(x, k: int, search: SearchConfig | None = None, nan_word=None):
+    """Row top-k of a CUDA float32 matrix enqueued on the current stream with
+    no host synchronisation (capturable in a CUDA graph): returns device
+    (values, indices).  NaN rows are not raised here -- pass a 1-element
+    int32 CUDA tensor as `nan_word` to receive the first offending row
+    (-1 when none) and check it when convenient.  Validation of shape and k
+    is done on the host as in batch_topk."""
+    torch = _require_cuda()
+    if not (_is_torch(x) and x.is_cuda):
+        raise ValueError("topk_device expects a CUDA tensor; use batch_topk for host input")
+    dm = _DeviceMatrix(x)
+    k = int(k)
+    if k < 1 or k > dm.m:
+        raise KOutOfRangeError(f"k must be in [1, {dm.m}], got {k}")
+    if nan_word is not None and (nan_word.dtype != torch.int32 or not nan_word.is_cuda or nan_word.numel() < 1):
+        raise ValueError("nan_word must be a CUDA int32 tensor with at least one element")
+    vals, idx, _, _ = dm.launch_topk(k, search or SearchConfig.exact(), False, nan_word=nan_word)
+    return vals, idx
+
+
 def exact_trace(matrix, k: int, search: SearchConfig | None = None):
     """Exit statistics only (_kernels.exact_trace_chunk, _kernels.py:217-231):
     (trace_iterations int32 (N,), trace_reasons int8 (N,))."""

@@ -25,7 +25,7 @@ from __future__ import annotations
 import torch
 
 from . import _native
-from .batch import BatchConfig, batch_topk
+from .batch import BatchConfig, batch_topk, topk_device
 from .select import SearchConfig
 
 
@@ -70,46 +70,55 @@ def gather_rows(dense: torch.Tensor, indices: torch.Tensor) -> torch.Tensor:
     return vals
 
 
+def _select(x, k, search, check_nan):
+    if check_nan:
+        res = batch_topk(x, BatchConfig(k=k, search=search))
+        return res.values, res.indices
+    return topk_device(x, k, search)  # no host sync: CUDA-graph capturable
+
+
 class _MaxK(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, k, search):
-        res = batch_topk(x.detach(), BatchConfig(k=k, search=search))
-        ctx.save_for_backward(res.indices)
+    def forward(ctx, x, k, search, check_nan):
+        values, indices = _select(x.detach(), k, search, check_nan)
+        ctx.save_for_backward(indices)
         ctx.m = int(x.shape[1])
-        ctx.mark_non_differentiable(res.indices)
-        return res.values, res.indices
+        ctx.mark_non_differentiable(indices)
+        return values, indices
 
     @staticmethod
     def backward(ctx, grad_values, _grad_indices):
         (indices,) = ctx.saved_tensors
         if grad_values is None:
-            return None, None, None
-        return scatter_rows(grad_values.contiguous(), indices, ctx.m), None, None
+            return None, None, None, None
+        return scatter_rows(grad_values.contiguous(), indices, ctx.m), None, None, None
 
 
 class _MaxKDense(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, k, search):
-        res = batch_topk(x.detach(), BatchConfig(k=k, search=search))
-        ctx.save_for_backward(res.indices)
-        return scatter_rows(res.values, res.indices, int(x.shape[1]))
+    def forward(ctx, x, k, search, check_nan):
+        values, indices = _select(x.detach(), k, search, check_nan)
+        ctx.save_for_backward(indices)
+        return scatter_rows(values, indices, int(x.shape[1]))
 
     @staticmethod
     def backward(ctx, grad_out):
         (indices,) = ctx.saved_tensors
-        return scatter_rows(gather_rows(grad_out, indices), indices, int(grad_out.shape[1])), None, None
+        return scatter_rows(gather_rows(grad_out, indices), indices, int(grad_out.shape[1])), None, None, None
 
 
-def maxk(x: torch.Tensor, k: int, search: SearchConfig | None = None):
+def maxk(x: torch.Tensor, k: int, search: SearchConfig | None = None, check_nan: bool = True):
     """Row top-k of a CUDA float32 matrix as (values, int32 indices); values
-    carry the gradient (scattered back to the selected columns)."""
-    return _MaxK.apply(x, int(k), search or SearchConfig.exact())
+    carry the gradient (scattered back to the selected columns).
+    check_nan=False skips the NaN read-back (no host sync per call; the op
+    can then be captured in a CUDA graph)."""
+    return _MaxK.apply(x, int(k), search or SearchConfig.exact(), bool(check_nan))
 
 
-def maxk_dense(x: torch.Tensor, k: int, search: SearchConfig | None = None) -> torch.Tensor:
+def maxk_dense(x: torch.Tensor, k: int, search: SearchConfig | None = None, check_nan: bool = True) -> torch.Tensor:
     """The MaxK nonlinearity in dense form: x with all but each row's top-k
     entries set to zero (gradient flows to the kept entries only)."""
-    return _MaxKDense.apply(x, int(k), search or SearchConfig.exact())
+    return _MaxKDense.apply(x, int(k), search or SearchConfig.exact(), bool(check_nan))
 
 
 def to_sparse_csr(values: torch.Tensor, indices: torch.Tensor, m: int) -> torch.Tensor:

@@ -87,3 +87,41 @@ def test_sparse_csr_view_spmm():
     assert torch.equal(csr.to_dense(), dense)
     w = torch.randn(m, 64, device="cuda")
     assert torch.allclose(torch.sparse.mm(csr, w), dense @ w, rtol=1e-4, atol=1e-4)
+
+
+def test_topk_device_is_sync_free_and_graph_capturable():
+    """topk_device / maxk(check_nan=False) enqueue without host syncs, so a
+    MaxK layer (top-k + scatter + SpMM-style matmul) captures into a CUDA
+    graph; replays equal eager results and the NaN word reports the row."""
+    n, m, k = 4096, 256, 32
+    x = torch.randn(n, m, device="cuda")
+    w = torch.randn(m, 64, device="cuda")
+    nan_word = torch.empty(1, dtype=torch.int32, device="cuda")
+    want_v, want_i = rtk.topk_device(x, k, nan_word=nan_word)
+    assert int(nan_word.item()) == -1
+    ref = rtk.batch_topk(x, rtk.BatchConfig(k=k))
+    assert torch.equal(want_v, ref.values) and torch.equal(want_i, ref.indices)
+
+    static_x = x.clone()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(2):  # warm-up outside capture (allocator, library load)
+            out = rtk.maxk_dense(static_x, k, check_nan=False) @ w
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        out = rtk.maxk_dense(static_x, k, check_nan=False) @ w
+    for trial in range(3):
+        static_x.copy_(torch.randn(n, m, device="cuda"))
+        g.replay()
+        torch.cuda.synchronize()
+        eager = rtk.maxk_dense(static_x, k) @ w
+        assert torch.equal(out, eager), trial
+
+    bad = x.clone()
+    bad[1234, 5] = float("nan")
+    rtk.topk_device(bad, k, nan_word=nan_word)
+    assert int(nan_word.item()) == 1234
+    with pytest.raises(rtk.KOutOfRangeError):
+        rtk.topk_device(x, m + 1)
