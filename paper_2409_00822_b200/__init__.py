@@ -32,6 +32,18 @@ from .errors import (  # noqa: F401
     TruncatedFileError,
     VerificationError,
 )
+from .experiments import (  # noqa: F401
+    DataGenSpec,
+    EarlyStopStats,
+    early_stop_experiment,
+    early_stop_grid,
+    early_stop_grid_matrix,
+    exit_iteration_grid,
+    exit_iteration_grid_matrix,
+    generate_matrix,
+    trial_block,
+    trial_row,
+)
 from .io import load_matrix, load_result, save_matrix, save_result, topk_file  # noqa: F401
 from .maxk import gather_rows, maxk, maxk_dense, scatter_rows, to_sparse_csr  # noqa: F401
 from .select import (  # noqa: F401
@@ -57,4 +69,6 @@ __all__ = [
     "TopKResult", "as_matrix", "as_row", "batch_topk", "chunk_ranges", "count_ge", "early_stop_topk",
     "exact_topk", "exact_trace", "min_max", "oracle_topk", "resolve_workers", "load_matrix", "load_result",
     "save_matrix", "save_result", "topk_file", "topk_device", "maxk", "maxk_dense", "scatter_rows", "gather_rows", "to_sparse_csr",
+    "DataGenSpec", "EarlyStopStats", "early_stop_experiment", "early_stop_grid", "early_stop_grid_matrix",
+    "exit_iteration_grid", "exit_iteration_grid_matrix", "generate_matrix", "trial_block", "trial_row",
 ]

@@ -81,8 +81,8 @@ int ctas_per_sm(const void* kernel, size_t smem, int threads) {
     return blocks;
 }
 
-int launch_flat(void (*kernel)(rtk::Args), const rtk::Args& a, cudaStream_t s) {
-    const long long total = a.n * (long long)a.m;
+int launch_flat(void (*kernel)(rtk::Args), const rtk::Args& a, cudaStream_t s, int per_item = 1) {
+    const long long total = a.n * (long long)a.m / per_item;
     long long grid = (total + kFlatThreads - 1) / kFlatThreads;
     const long long cap = (long long)device_sms() * 8;
     if (grid > cap) grid = cap;
@@ -158,7 +158,12 @@ int rowtopk_common(int mode, const float* x, int64_t n, int64_t m, int64_t ldx, 
     a.eps_rel = eps_rel;
     a.hard_cap = hard_cap;
     a.max_iter = max_iter;
-    if (k == m) return launch_flat(rtk::full_copy_kernel, a, s);  // _kernels.py:173-179
+    if (k == m) {  // _kernels.py:173-179
+        const bool vec = m % 4 == 0 && ldx % 4 == 0 && (!vals || ldo % 4 == 0) &&
+                         ((uintptr_t)x & 15u) == 0 && ((uintptr_t)vals & 15u) == 0 && ((uintptr_t)idx & 15u) == 0 &&
+                         n * (m / 4) < 0xffffffffLL;
+        return launch_flat(vec ? rtk::full_copy_vec4_kernel : rtk::full_copy_kernel, a, s, vec ? 4 : 1);
+    }
     switch (mode) {
         case rtk::kExact: return rtk_dispatch_exact(a, s);
         case rtk::kEarly: return rtk_dispatch_early(a, s);

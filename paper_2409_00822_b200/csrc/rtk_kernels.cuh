@@ -1066,6 +1066,39 @@ __global__ void __launch_bounds__(256) full_copy_kernel(Args a) {
     }
 }
 
+// k == M with 16-byte aligned rows (M, ldx, ldo multiples of 4): one float4
+// of values and one int4 of indices per item, 32-bit row arithmetic
+// (the host guarantees n * M / 4 < 2^32), streaming loads and stores.
+__device__ __forceinline__ void copy_item4(const Args& a, unsigned r, unsigned c, float4 x) {
+    const unsigned long long o = (unsigned long long)r * a.ldo + c;
+    if (a.vals) {
+        __stcs(reinterpret_cast<float4*>(a.vals + o), x);
+        __stcs(reinterpret_cast<int4*>(a.idx + o), make_int4((int)c, (int)c + 1, (int)c + 2, (int)c + 3));
+    }
+    if ((x.x != x.x || x.y != x.y || x.z != x.z || x.w != x.w) && a.nan_row) atomicMin(a.nan_row, r);
+    if (c == 0u) {
+        if (a.iters) a.iters[r] = 0;
+        if (a.reasons) a.reasons[r] = (signed char)kExitDegenerateRow;
+    }
+}
+
+__global__ void __launch_bounds__(256) full_copy_vec4_kernel(Args a) {
+    const unsigned m4 = (unsigned)a.m >> 2;
+    const unsigned total = (unsigned)a.n * m4;
+    const unsigned stride = gridDim.x * blockDim.x;
+    // two items per thread and iteration, both loads issued before the stores
+    for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += 2u * stride) {
+        const unsigned e2 = e + stride;
+        const unsigned r = e / m4, c = 4u * (e - r * m4);
+        const unsigned r2 = e2 / m4, c2 = 4u * (e2 - r2 * m4);
+        const float4 x = __ldcs(reinterpret_cast<const float4*>(a.x + (unsigned long long)r * a.ldx + c));
+        float4 x2 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (e2 < total) x2 = __ldcs(reinterpret_cast<const float4*>(a.x + (unsigned long long)r2 * a.ldx + c2));
+        copy_item4(a, r, c, x);
+        if (e2 < total) copy_item4(a, r2, c2, x2);
+    }
+}
+
 // NaN scan (batch.py:37-39) as a standalone pass.
 __global__ void __launch_bounds__(256) nan_scan_kernel(Args a) {
     const long long total = a.n * (long long)a.m;

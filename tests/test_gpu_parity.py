@@ -327,3 +327,36 @@ def test_large_offsets_sampled_vs_oracle(oracle_lib):
         assert np.array_equal(res.trace_iterations[rows].cpu().numpy(), t)
     del x
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("m", [1, 3, 4, 128, 130, 256])
+def test_k_equals_m_copy_paths(m):
+    """k == M (_kernels.py:173-179): the row itself with indices 0..M-1 and
+    trace (0, DEGENERATE_ROW), on the vectorised copy (M % 4 == 0, aligned)
+    and the scalar copy (odd M, strided views, unaligned outputs); NaN rows
+    still raise with the first offending row."""
+    rng = np.random.default_rng(m)
+    n = 70_001
+    x = rng.standard_normal((n, m), dtype=np.float32)
+    x[5, 0] = -0.0
+    want_i = np.broadcast_to(np.arange(m, dtype=np.int32), (n, m))
+    for xd in (torch.from_numpy(x).cuda(), torch.from_numpy(np.pad(x, ((0, 0), (0, 3)))).cuda()[:, :m]):
+        for search in (rtk.SearchConfig.exact(), rtk.SearchConfig.early_stop(4)):
+            res = rtk.batch_topk(xd, rtk.BatchConfig(k=m, search=search, collect_traces=True))
+            assert np.array_equal(_bits(_np(res.values)), _bits(x))
+            assert np.array_equal(_np(res.indices), want_i)
+            assert (_np(res.trace_iterations) == 0).all() and (_np(res.trace_reasons) == 5).all()
+    # outputs at an odd ldo through the C ABI (scalar path) and via numpy in
+    vals = torch.full((n, m + 1), 7.0, device="cuda")
+    idx = torch.full((n, m + 1), -1, dtype=torch.int32, device="cuda")
+    xd = torch.from_numpy(x).cuda()
+    rtk._native.call("rtk_rowtopk_exact_f32", xd.data_ptr(), n, m, m, m, 0.0, 64, vals.data_ptr(), idx.data_ptr(),
+                     m + 1, None, None, None, torch.cuda.current_stream().cuda_stream)
+    assert np.array_equal(_bits(vals[:, :m].cpu().numpy()), _bits(x))
+    assert np.array_equal(idx[:, :m].cpu().numpy(), want_i)
+    assert (vals[:, m] == 7.0).all() and (idx[:, m] == -1).all()
+    bad = x.copy()
+    bad[n - 3, m - 1] = np.nan
+    bad[n - 2, 0] = np.nan
+    with pytest.raises(rtk.NaNInputError, match=str(n - 3)):
+        rtk.batch_topk(torch.from_numpy(bad).cuda(), rtk.BatchConfig(k=m))

@@ -23,6 +23,7 @@ run_full c2_early early
 run_full m1024_exact exact 1048576:1024:64
 run_full m1024_early early 1048576:1024:64
 run_full m512_early early 1048576:512:64
+run_full m4096_exact exact 262144:4096:64
 timeout 900 python tools/sweep_bench.py --out $OUT/sweep.json > $OUT/sweep.log 2>&1
 timeout 600 python tools/maxk_bench.py > $OUT/maxk_bench.json 2> $OUT/maxk_bench.err
 timeout 600 python tools/file_bench.py /dev/shm > $OUT/file_bench_tmpfs.json 2> $OUT/file_bench.err
