@@ -20,6 +20,7 @@ stride) and the results stay on their device as torch tensors.
 from __future__ import annotations
 
 import os
+import warnings
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -58,7 +59,11 @@ def _is_torch(x) -> bool:
 def _host_matrix(values) -> np.ndarray:
     """The conversion + shape checks of as_matrix (batch.py:30-36), on the host."""
     if _is_torch(values):
-        values = values.detach().cpu().numpy()
+        torch = _torch()
+        t = values.detach()
+        if t.dtype == torch.bfloat16:  # no numpy dtype; the widening to float32 is exact
+            t = t.to(torch.float32)
+        values = t.cpu().numpy()
     m = np.ascontiguousarray(values, dtype=np.float32)
     if m.ndim != 2:
         raise DimensionMismatchError(f"expected a 2-D matrix, got shape {m.shape}")
@@ -81,7 +86,9 @@ class _DeviceMatrix:
                 if t.numel() == 0:
                     raise EmptyRowError(f"matrix must be at least 1 x 1, got {tuple(t.shape)}")
             else:
-                t = torch.from_numpy(_host_matrix(values))
+                with warnings.catch_warnings():  # read-only arrays (memmaps) are only read from
+                    warnings.simplefilter("ignore", UserWarning)
+                    t = torch.from_numpy(_host_matrix(values))
             self.x = t.to(torch.device("cuda", torch.cuda.current_device()),
                           non_blocking=t.is_pinned())
         else:
@@ -361,7 +368,9 @@ def _host_tensor(matrix):
         if t.numel() == 0:
             raise EmptyRowError(f"matrix must be at least 1 x 1, got {tuple(t.shape)}")
         return t
-    return torch.from_numpy(_host_matrix(matrix))
+    with warnings.catch_warnings():  # read-only arrays (memmaps) are only read from
+        warnings.simplefilter("ignore", UserWarning)
+        return torch.from_numpy(_host_matrix(matrix))
 
 
 def batch_topk(matrix, cfg: BatchConfig) -> BatchResult:

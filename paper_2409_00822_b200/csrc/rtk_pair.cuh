@@ -25,6 +25,13 @@ namespace rtk {
 #ifndef RTK_PAIR_MIN_CTAS
 #define RTK_PAIR_MIN_CTAS 2  // __launch_bounds__ min CTAs per SM (caps registers at 64)
 #endif
+#ifndef RTK_PAIR_MIN_CTAS_E4
+#define RTK_PAIR_MIN_CTAS_E4 2  // the same for E = 4 (M <= 128)
+#endif
+template <int E>
+struct PairMinCtas {
+    static constexpr int value = E <= 4 ? RTK_PAIR_MIN_CTAS_E4 : RTK_PAIR_MIN_CTAS;
+};
 
 // Inclusive warp prefix sum (SHFL.UP's in-range predicate guards the add);
 // not volatile, so the compiler may schedule other work between the steps.
@@ -198,7 +205,7 @@ __device__ __forceinline__ void process_pair(const Row& A, const Row& B, unsigne
 // double buffering of the pair (the roles of the two tile pairs alternate
 // between the two unrolled halves).
 template <int MODE, int E, bool MASKED, bool WIDE>
-__global__ void __launch_bounds__(RTK_CTA_THREADS, RTK_PAIR_MIN_CTAS) rowtopk_pair_kernel(Args a) {
+__global__ void __launch_bounds__(RTK_CTA_THREADS, PairMinCtas<E>::value) rowtopk_pair_kernel(Args a) {
     using Row = LaneRow<E, MASKED, WIDE>;
     extern __shared__ __align__(16) float smem[];
     const int lane = threadIdx.x & 31;

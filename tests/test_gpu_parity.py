@@ -360,3 +360,36 @@ def test_k_equals_m_copy_paths(m):
     bad[n - 2, 0] = np.nan
     with pytest.raises(rtk.NaNInputError, match=str(n - 3)):
         rtk.batch_topk(torch.from_numpy(bad).cuda(), rtk.BatchConfig(k=m))
+
+
+def test_input_dtypes_convert_like_as_matrix(oracle_lib):
+    """as_matrix (batch.py:30-36) converts any input to contiguous float32
+    before the search: float64 (rounded), float16, integers, bools, nested
+    lists, Fortran-ordered arrays, and torch tensors of those dtypes (host and
+    CUDA, incl. bfloat16) give the oracle's result on the float32 image."""
+    rng = np.random.default_rng(77)
+    n, m, k = 1001, 200, 17
+    base = rng.standard_normal((n, m)) * 3.0
+    inputs = [
+        base,  # float64: rounds to nearest float32 like ndarray.astype
+        base.astype(np.float16),
+        np.round(base * 10).astype(np.int64),
+        np.round(base).astype(np.int16),
+        base > 0.5,
+        np.asfortranarray(base.astype(np.float32)),
+        base[:, ::-1],
+    ]
+    tinputs = [torch.from_numpy(base), torch.from_numpy(base).to(torch.bfloat16),
+               torch.from_numpy(base).to(torch.float16), torch.from_numpy(np.round(base * 10).astype(np.int32))]
+    for search in (rtk.SearchConfig.exact(), rtk.SearchConfig.early_stop(3)):
+        mode = "exact" if search.mode is rtk.SearchMode.EXACT else "early"
+        for x in inputs + tinputs + [t.cuda() for t in tinputs] + [base[:5].tolist()]:
+            if isinstance(x, torch.Tensor):
+                x32 = x.to(torch.float32).cpu().numpy()
+            else:
+                x32 = np.ascontiguousarray(x, dtype=np.float32)
+            want = oracle_lib.ref_batch(x32, k, mode, max_iter=3)
+            res = rtk.batch_topk(x, rtk.BatchConfig(k=k, search=search))
+            ctx = (type(x).__name__, getattr(x, "dtype", None), mode)
+            assert np.array_equal(_np(res.indices), want[1]), ctx
+            assert np.array_equal(_bits(_np(res.values)), _bits(want[0])), ctx
