@@ -23,15 +23,26 @@ namespace rtk {
 #define RTK_BIG_THREADS 256
 #endif
 
-// Minimum resident CTAs (of RTK_BIG_THREADS) per SM requested from ptxas:
-// caps registers at ~64 (E = 24..32; ~85 with masking), ~51 (E = 16..20), ~42 (E = 12).
+// Threads per CTA and minimum resident CTAs per SM requested from ptxas.
+// E <= 32 (256 threads): caps registers at ~64 (E = 24..32; ~85 with
+// masking), ~51 (E = 16..20), ~42 (E = 12).  Rows past 1024 columns keep
+// one warp per row with E = 48..128 elements per lane (128 threads): the cap
+// is about E + 64 registers (16 resident warps at E <= 64, 12 at 96, 8 at 128).
+#ifndef RTK_BIG_WIDE_THREADS
+#define RTK_BIG_WIDE_THREADS 256  // CTA size for E > 32
+#endif
+template <int E>
+struct BigThreads {
+    static constexpr int value = E > 32 ? RTK_BIG_WIDE_THREADS : RTK_BIG_THREADS;
+};
 template <int E, bool MASKED>
 struct BigMinCtas {
-    static constexpr int value = E <= 12 ? 6 : (E <= 20 ? 5 : (MASKED ? 3 : 4));
+    static constexpr int wide = 65536 / (BigThreads<E>::value * (E + 64));
+    static constexpr int value = E <= 12 ? 6 : (E <= 20 ? 5 : (E <= 32 ? (MASKED ? 3 : 4) : (wide > 0 ? wide : 1)));
 };
 
 template <int MODE, int E, bool MASKED, bool TRACES>
-__global__ void __launch_bounds__(RTK_BIG_THREADS, BigMinCtas<E, MASKED>::value) rowtopk_big_kernel(Args a) {
+__global__ void __launch_bounds__(BigThreads<E>::value, BigMinCtas<E, MASKED>::value) rowtopk_big_kernel(Args a) {
     using Row = LaneRowCut<E, MASKED>;
     constexpr int D = RTK_BIG_DEPTH;
     extern __shared__ __align__(16) float smem[];
@@ -48,6 +59,11 @@ __global__ void __launch_bounds__(RTK_BIG_THREADS, BigMinCtas<E, MASKED>::value)
     if (r >= n) return;
     const unsigned ldx_b = (unsigned)a.ldx * 4u;
     const bool fp = a.eps_rel == 0.0;
+    if constexpr (MASKED) {  // padding chunks of the ring: NaN once (load_smem_prefilled)
+#pragma unroll
+        for (int d = 0; d < D; ++d) Row::fill_slot_nan(ring + d * Row::kRowBytes, lane);
+        __syncwarp();
+    }
     // prologue: rows r, r + nw, ..., r + (D-1) nw
 #pragma unroll
     for (int d = 0; d < D; ++d) {
@@ -61,12 +77,13 @@ __global__ void __launch_bounds__(RTK_BIG_THREADS, BigMinCtas<E, MASKED>::value)
         cp_async_wait<D - 1>();  // this lane's copies of this row have landed ...
         __syncwarp();            // ... and (chunks go to their owner lanes) every lane's
         const unsigned sl = ring + slot * Row::kRowBytes;
-        row.load_smem(sl, a.m, lane);
+        row.load_smem_prefilled(sl, lane);
         const unsigned long long rpre = (unsigned long long)r + (unsigned long long)D * nw;
         // refill after the tile has been read (the token orders the LDGSTS after the LDS)
         process_row<MODE, TRACES>(row, r, a, lane, sbase, fp, [&](unsigned tok) {
             __syncwarp();  // every lane has read its tile out of the slot before any refill lands
-            if (rpre < n) Row::stage_async(row_ptr(a.x, (unsigned)rpre + (tok & a.opaque_zero), ldx_b), a.m, lane, sl);
+            const unsigned salt = tok & a.opaque_zero;
+            if (rpre < n) Row::stage_async(row_ptr(a.x, (unsigned)rpre + salt, ldx_b), a.m, lane, sl, salt);
             cp_async_commit();
         });
         if ((unsigned long long)r + nw >= n) break;

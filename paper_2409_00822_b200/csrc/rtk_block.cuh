@@ -1,20 +1,22 @@
-// rtk_block.cuh -- one CTA per row for long rows (1024 < M <= 8192 on the
-// vectorised path; the reference's validated regime ends at 8192 columns,
-// batch.py:27).
+// rtk_block.cuh -- one CTA per row for the longest rows (4096 < M <= 8192 on
+// the vectorised path; the reference's validated regime ends at 8192
+// columns, batch.py:27).  Rows up to 4096 columns stay one warp per row
+// (rtk_big.cuh with E up to 128 elements per lane), which measured faster:
+// every reduction here costs a block barrier.
 //
-// W warps share a row: thread t of the CTA holds the E = 32 consecutive
-// elements [t E, (t+1) E) in registers (the LaneRow layout with the lane
-// index taken over the whole CTA), so the per-step work of a warp stays that
-// of the 1024-column kernel.  Row-level values combine in two stages: a warp
-// collective (REDUX / CREDUX / shuffle scan) and a shared-memory exchange of
-// the W warp results behind one __syncthreads per reduction (double-buffered
-// slots, so no second barrier is needed before the next step overwrites
-// them).  Every thread ends up with the row's value, so the general search
-// code (row_body: exact and early-stop loops, every exit rule, traces, the
-// fill branch) runs unchanged on BlockRow.  Each warp streams its slice of
-// the next row into a shared-memory slot with cp.async while the current row
-// is searched; selected (value, index) pairs are staged in shared memory up
-// to position k and written by the whole CTA.
+// W warps share a row: thread t of the CTA holds the E = 8192 / (32 W)
+// consecutive elements [t E, (t+1) E) in registers (the LaneRow layout with
+// the lane index taken over the whole CTA), so the per-step work of a warp
+// stays that of the long-row kernel.  Row-level values combine in two
+// stages: a warp collective (REDUX / CREDUX / shuffle scan) and a
+// shared-memory exchange of the W warp results behind one __syncthreads per
+// reduction (double-buffered slots, so no second barrier is needed before the
+// next step overwrites them).  Every thread ends up with the row's value, so
+// the general search code (row_body: exact and early-stop loops, every exit
+// rule, traces, the fill branch) runs unchanged on BlockRow.  Each warp
+// streams its slice of the next row into a shared-memory slot with cp.async
+// while the current row is searched; selected (value, index) pairs are
+// staged in shared memory up to position k and written by the whole CTA.
 #pragma once
 
 #include "rtk_kernels.cuh"
@@ -169,16 +171,18 @@ struct BlockRow {
     }
 };
 
-template <int W>
+// E = 32: caps registers at ~85; wider tiles: about E + 64 registers.
+template <int W, int E>
 struct BlockMinCtas {
-    static constexpr int value = 768 / (W * 32) > 0 ? 768 / (W * 32) : 1;  // caps registers at ~85
+    static constexpr int raw = E <= 32 ? 768 / (W * 32) : 65536 / (W * 32 * (E + 64));
+    static constexpr int value = raw > 0 ? raw : 1;
 };
 
 // Persistent loop over rows (CTA per row).  Shared memory: k staged pairs,
-// then one cp.async slot per warp for its slice of the next row.
-template <int MODE, int W, bool TRACES>
-__global__ void __launch_bounds__(W * 32, BlockMinCtas<W>::value) rowtopk_block_kernel(Args a) {
-    constexpr int E = 32;
+// then one cp.async slot per warp for its slice of the next row (padding
+// chunks NaN-filled once, as in the long-row kernel).
+template <int MODE, int W, int E, bool TRACES>
+__global__ void __launch_bounds__(W * 32, BlockMinCtas<W, E>::value) rowtopk_block_kernel(Args a) {
     using Row = BlockRow<E, W, true>;
     using Tile = typename Row::Tile;
     extern __shared__ __align__(16) float smem[];
@@ -194,19 +198,21 @@ __global__ void __launch_bounds__(W * 32, BlockMinCtas<W>::value) rowtopk_block_
     const unsigned ldx_b = (unsigned)a.ldx * 4u;
     const int mw = a.m - w * 32 * E;  // columns of the row from this warp's slice on
     const bool fp = a.eps_rel == 0.0;
+    Tile::fill_slot_nan(slot, lane);
+    __syncwarp();
     Tile::stage_async(row_ptr(a.x, r, ldx_b) + w * 32 * E, mw, lane, slot);
     cp_async_commit();
     Row row;
     for (;;) {
         cp_async_wait<0>();
         __syncwarp();  // chunks land in their owner lanes' parts of the slot
-        row.tile.load_smem(slot, mw, lane);
+        row.tile.load_smem_prefilled(slot, lane);
         const unsigned long long rn = (unsigned long long)r + gridDim.x;
         process_row<MODE, TRACES>(row, r, a, lane, sbase, fp, [&](unsigned tok) {
             __syncwarp();  // every lane has read its part of the slot
+            const unsigned salt = tok & a.opaque_zero;
             if (rn < n)
-                Tile::stage_async(row_ptr(a.x, (unsigned)rn + (tok & a.opaque_zero), ldx_b) + w * 32 * E, mw,
-                                  lane, slot);
+                Tile::stage_async(row_ptr(a.x, (unsigned)rn + salt, ldx_b) + w * 32 * E, mw, lane, slot, salt);
             cp_async_commit();
         });
         if (rn >= n) break;

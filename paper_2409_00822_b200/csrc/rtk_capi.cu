@@ -61,10 +61,12 @@ int device_sms() {
 }
 
 // Occupancy (CTAs per SM) of one kernel instantiation at a dynamic shared
-// memory size, cached per (device, kernel, smem); kernels needing more than
-// 48 KB of dynamic shared memory are opted in once.
+// memory size, cached per (device, kernel, smem, threads).  Kernels needing
+// more than 48 KB of dynamic shared memory are opted in to the largest size
+// requested so far (never lowered, so every cached size stays launchable).
 std::mutex g_occ_mu;
 std::map<std::tuple<int, const void*, size_t>, int> g_occ;
+std::map<std::pair<int, const void*>, size_t> g_smem_optin;
 
 int ctas_per_sm(const void* kernel, size_t smem, int threads) {
     int dev = 0;
@@ -73,7 +75,13 @@ int ctas_per_sm(const void* kernel, size_t smem, int threads) {
     auto key = std::make_tuple(dev, kernel, smem + ((size_t)threads << 40));
     auto it = g_occ.find(key);
     if (it != g_occ.end()) return it->second;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (smem > 48 * 1024) {
+        size_t& cur = g_smem_optin[std::make_pair(dev, kernel)];
+        if (smem > cur) {
+            cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cur = smem;
+        }
+    }
     int blocks = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, threads, smem) != cudaSuccess || blocks < 1)
         blocks = 1;

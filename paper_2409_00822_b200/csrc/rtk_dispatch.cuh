@@ -39,6 +39,7 @@ int fail(int code, const char* fmt, T... args) {
 #endif
 constexpr int kThreads = RTK_CTA_THREADS;  // threads per CTA of the row kernels
 constexpr int kFlatThreads = 256;         // threads per CTA of the elementwise kernels
+constexpr size_t kMaxSmem = 227 * 1024;   // dynamic shared memory per CTA (sm_100 opt-in limit)
 
 
 template <class K>
@@ -80,9 +81,14 @@ int launch_reg(const rtk::Args& a, cudaStream_t s) {
 template <int MODE, int E, bool MASKED, bool TRACES>
 int launch_big_kernel(const rtk::Args& a, cudaStream_t s) {
     using Row = rtk::LaneRowCut<E, MASKED>;
-    constexpr int wpc = RTK_BIG_THREADS / 32;
-    const size_t smem = (size_t)wpc * (Row::stage_bytes(a.k) + RTK_BIG_DEPTH * Row::kRowBytes);
-    return launch_rows(rtk::rowtopk_big_kernel<MODE, E, MASKED, TRACES>, a, s, smem, RTK_BIG_THREADS);
+    // warps per CTA: BigThreads, fewer when k pairs + ring of 8 warps would
+    // not fit in shared memory (the kernel reads its warp count from blockDim)
+    const size_t per_warp = Row::stage_bytes(a.k) + RTK_BIG_DEPTH * Row::kRowBytes;
+    int wpc = rtk::BigThreads<E>::value / 32;
+    while (wpc > 1 && (size_t)wpc * per_warp > kMaxSmem) --wpc;
+    const int threads = 32 * wpc;
+    const size_t smem = (size_t)wpc * per_warp;
+    return launch_rows(rtk::rowtopk_big_kernel<MODE, E, MASKED, TRACES>, a, s, smem, threads);
 }
 
 // TMA staging for unmasked long rows with E = 16 / 32 (rtk_big.cuh).
@@ -165,22 +171,32 @@ int launch_lane(const rtk::Args& a, cudaStream_t s) {
     if constexpr (E >= RTK_BIG_MIN_E) {
         if (a.m == 32 * E) return launch_big<MODE, E, false>(a, s);
         return launch_big<MODE, E, true>(a, s);
+    } else {
+        // staging buffer per warp: row copy + 32*E indices (no selection in trace mode)
+        const size_t smem = MODE == rtk::kTrace ? 0 : (size_t)(kThreads / 32) * rtk::LaneRow<E, false>::kStageBytes;
+        const bool wide = (reinterpret_cast<uintptr_t>(a.x) & 31) == 0 && a.ldx % 8 == 0;  // 256-bit loads
+        if (a.m == 32 * E && wide) return launch_row_kernel<MODE, rtk::LaneRow<E, false, true>>(a, s, smem);
+        if (a.m == 32 * E) return launch_row_kernel<MODE, rtk::LaneRow<E, false, false>>(a, s, smem);
+        return launch_row_kernel<MODE, rtk::LaneRow<E, true, false>>(a, s, smem);
     }
-    // staging buffer per warp: row copy + 32*E indices (no selection in trace mode)
-    const size_t smem = MODE == rtk::kTrace ? 0 : (size_t)(kThreads / 32) * rtk::LaneRow<E, false>::kStageBytes;
-    const bool wide = (reinterpret_cast<uintptr_t>(a.x) & 31) == 0 && a.ldx % 8 == 0;  // 256-bit loads
-    if (a.m == 32 * E && wide) return launch_row_kernel<MODE, rtk::LaneRow<E, false, true>>(a, s, smem);
-    if (a.m == 32 * E) return launch_row_kernel<MODE, rtk::LaneRow<E, false, false>>(a, s, smem);
-    return launch_row_kernel<MODE, rtk::LaneRow<E, true, false>>(a, s, smem);
 }
 
-// Long rows (rtk_block.cuh): one CTA of W warps per row, 1024 < M <= 8192.
-template <int MODE, int W, bool TRACES>
+// Longest rows (rtk_block.cuh): one CTA of W warps per row, 4096 < M <= 8192;
+// each lane holds E = CAP / (32 W) elements (CAP = 6144 or 8192 columns).
+// W = 2 measured best in exact mode, W = 4 with early stop.
+#ifdef RTK_BLOCK_W
+template <int MODE>
+constexpr int kBlockW = RTK_BLOCK_W;
+#else
+template <int MODE>
+constexpr int kBlockW = MODE == rtk::kEarly ? 4 : 2;
+#endif
+template <int MODE, int W, int E, bool TRACES>
 int launch_block_kernel(const rtk::Args& a, cudaStream_t s) {
-    using Tile = rtk::LaneRow<32, true, false>;
+    using Tile = rtk::LaneRow<E, true, false>;
     const int threads = W * 32;
     const size_t smem = (((size_t)8 * a.k + 15) & ~(size_t)15) + (size_t)W * Tile::kRowBytes;
-    auto kernel = rtk::rowtopk_block_kernel<MODE, W, TRACES>;
+    auto kernel = rtk::rowtopk_block_kernel<MODE, W, E, TRACES>;
     long long grid = (long long)rtk_device_sms() * rtk_ctas_per_sm(reinterpret_cast<const void*>(kernel), smem, threads);
     if (grid > a.n) grid = a.n;
     if (grid < 1) grid = 1;
@@ -190,28 +206,30 @@ int launch_block_kernel(const rtk::Args& a, cudaStream_t s) {
     return RTK_OK;
 }
 
-template <int MODE, int W>
-int launch_block(const rtk::Args& a, cudaStream_t s) {
+template <int MODE, int W, int E>
+int launch_block_e(const rtk::Args& a, cudaStream_t s) {
     if constexpr (MODE == rtk::kTrace) {
-        return launch_block_kernel<MODE, W, true>(a, s);
+        return launch_block_kernel<MODE, W, E, true>(a, s);
     } else {
         if ((a.iters != nullptr) != (a.reasons != nullptr))
             return fail(RTK_EINVAL, "iters and reasons must be both NULL or both non-NULL");
-        if (a.iters != nullptr) return launch_block_kernel<MODE, W, true>(a, s);
-        return launch_block_kernel<MODE, W, false>(a, s);
+        if (a.iters != nullptr) return launch_block_kernel<MODE, W, E, true>(a, s);
+        return launch_block_kernel<MODE, W, E, false>(a, s);
     }
+}
+
+template <int MODE, int W>
+int launch_block(const rtk::Args& a, cudaStream_t s) {
+    if (a.m <= 6144) return launch_block_e<MODE, W, 6144 / (32 * W)>(a, s);
+    return launch_block_e<MODE, W, 8192 / (32 * W)>(a, s);
 }
 
 template <int MODE>
 int dispatch(const rtk::Args& a, cudaStream_t s) {
     const int m = a.m;
     const bool vec4 = (m % 4 == 0) && (a.ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
-#ifdef RTK_TUNE_BLOCK  // tuning builds: only the CTA-per-row kernels (M > 1024)
-    if (m > 1024 && m <= 8192 && vec4) {
-        if (m <= 2048) return launch_block<MODE, 2>(a, s);
-        if (m <= 4096) return launch_block<MODE, 4>(a, s);
-        return launch_block<MODE, 8>(a, s);
-    }
+#ifdef RTK_TUNE_BLOCK  // tuning builds: only the CTA-per-row kernel (M > 4096)
+    if (m > 4096 && m <= 8192 && vec4) return launch_block<MODE, kBlockW<MODE>>(a, s);
     return launch_row_kernel<MODE, rtk::GlobalRow>(a, s, 0);
 #elif defined(RTK_TUNE_E)  // tuning builds: only one register-tile width (fast to compile)
     if (m <= 1024 && vec4 && (m + 127) / 128 * 4 == RTK_TUNE_E) return launch_lane<MODE, RTK_TUNE_E>(a, s);
@@ -239,11 +257,14 @@ int dispatch(const rtk::Args& a, cudaStream_t s) {
         if (c <= 16) return launch_reg<MODE, 1, 16>(a, s);
         return launch_reg<MODE, 1, 32>(a, s);
     }
-    if (m <= 8192 && vec4) {
-        if (m <= 2048) return launch_block<MODE, 2>(a, s);
-        if (m <= 4096) return launch_block<MODE, 4>(a, s);
-        return launch_block<MODE, 8>(a, s);
+    if (m <= 4096 && vec4) {
+        // still one warp per row: E = 48 / 64 / 96 / 128 elements per lane
+        if (m <= 1536) return launch_lane<MODE, 48>(a, s);
+        if (m <= 2048) return launch_lane<MODE, 64>(a, s);
+        if (m <= 3072) return launch_lane<MODE, 96>(a, s);
+        return launch_lane<MODE, 128>(a, s);
     }
+    if (m <= 8192 && vec4) return launch_block<MODE, kBlockW<MODE>>(a, s);  // CTA per row
     return launch_row_kernel<MODE, rtk::GlobalRow>(a, s, 0);
 #endif
 }

@@ -399,25 +399,33 @@ struct LaneRow {
     // [512 g + 16 l, +16) of the row) and sends each 16-byte chunk to its
     // owner lane's slot: element e = 128 g + 4 l lives in lane e / E, chunk
     // (e % E) / 4 (constant divisors; for E | 128 the offsets are
-    // base + g * const).  Chunks past M are zero-filled (M % 4 == 0 here).
+    // base + g * const).  Chunks past M are skipped (M % 4 == 0 here).
     __device__ __forceinline__ static unsigned slot_offset(int lane) { return (unsigned)lane * kLaneStride; }
 
-    __device__ __forceinline__ static void stage_async(const float* __restrict__ p, int m, int lane, unsigned slot) {
+    // salt: 0 at run time but opaque to the compiler (token & opaque_zero);
+    // it keeps the per-chunk offsets and masks from being hoisted out of the
+    // row loop, where E > 32 would hold kChunks of them live (and spill).
+    __device__ __forceinline__ static void stage_async(const float* __restrict__ p, int m, int lane, unsigned slot,
+                                                       unsigned salt = 0u) {
         const float* src = p + 4 * lane;
+        const unsigned e0 = 4u * (unsigned)lane + salt;
 #pragma unroll
         for (int g = 0; g < (int)kChunks; ++g) {
-            const unsigned e = 128u * g + 4u * (unsigned)lane;
+            const unsigned e = 128u * g + e0;
             const unsigned dst = slot + (e / E) * kLaneStride + 16u * ((e % E) / 4u);
-            cp_async16(dst, src + 128 * g, (!MASKED || (int)e < m) ? 16u : 0u);
+            // chunks past M are not copied (load_smem masks those slots), so
+            // every copy has the immediate size 16 and no per-chunk register
+            if (!MASKED || (int)e < m) cp_async16(dst, src + 128 * g, 16u);
         }
     }
 
     __device__ __forceinline__ void load_smem(unsigned slot, int m, int lane) {
         const unsigned src = slot + slot_offset(lane);
+        const int nv = m - lane * E;  // real slots of this lane (MASKED)
 #pragma unroll
         for (int g = 0; g < E / 4; ++g) {
             const float4 q = lds128(src + 16u * g);
-            const bool ok = valid(lane, 4 * g, m);
+            const bool ok = !MASKED || 4 * g < nv;
             const float nan = __int_as_float(0x7fffffff);
             v[4 * g] = ok ? q.x : nan;
             v[4 * g + 1] = ok ? q.y : nan;
@@ -426,13 +434,43 @@ struct LaneRow {
         }
     }
 
+    // Unmasked read of a slot whose padding chunks hold NaN already (see
+    // fill_slot_nan): no per-element select, so the LDS results are the tile.
+    __device__ __forceinline__ void load_smem_prefilled(unsigned slot, int lane) {
+        const unsigned src = slot + slot_offset(lane);
+#pragma unroll
+        for (int g = 0; g < E / 4; ++g) {
+            const float4 q = lds128(src + 16u * g);
+            v[4 * g] = q.x; v[4 * g + 1] = q.y; v[4 * g + 2] = q.z; v[4 * g + 3] = q.w;
+        }
+    }
+    // NaN into every chunk of a slot (stage_async never writes the chunks past
+    // M, so they stay NaN for every row of the launch).
+    __device__ __forceinline__ static void fill_slot_nan(unsigned slot, int lane) {
+        const float nan = __int_as_float(0x7fffffff);
+#pragma unroll 1
+        for (unsigned i = (unsigned)lane; i < kRowBytes / 16u; i += 32u)
+            asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};" ::"r"(slot + 16u * i), "f"(nan) : "memory");
+    }
+
     __device__ __forceinline__ void lane_min_max(int m, int lane, float& mn, float& mx) const {
         mn = __int_as_float(0x7f800000);
         mx = __int_as_float(0xff800000);
+        if constexpr (MASKED) {
+            // padding slots (NaN) are a suffix of the lane's slots; fmin_nan
+            // must not see them
+            const int nv = m - lane * E;
 #pragma unroll
-        for (int q = 0; q < E; ++q) {
-            if (valid(lane, q, m)) mn = fmin_nan(mn, v[q]);
-            mx = fmaxf(mx, v[q]);
+            for (int q = 0; q < E; ++q) {
+                mn = fmin_nan(mn, q < nv ? v[q] : mn);
+                mx = fmaxf(mx, v[q]);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < E; ++q) {
+                mn = fmin_nan(mn, v[q]);
+                mx = fmaxf(mx, v[q]);
+            }
         }
     }
 
@@ -594,25 +632,23 @@ struct LaneRowCut : LaneRow<E, MASKED, false> {
         return sink;
     }
 
+    // (cold; the compares are redone in the second pass rather than kept
+    // as 2E predicates, which would raise the register bound of the kernel)
     __device__ __forceinline__ void select_fill(float t, float lo, int need, int k, unsigned sbase, int lane) const {
-        bool pa[E], pb[E];
         unsigned packed = 0;
 #pragma unroll
-        for (int q = 0; q < E; ++q) {
-            pa[q] = v[q] >= t;
-            pb[q] = (lo <= v[q]) && (v[q] < t);
-            packed += (pa[q] ? 1u : 0u) + (pb[q] ? 0x10000u : 0u);
-        }
+        for (int q = 0; q < E; ++q)
+            packed += (v[q] >= t ? 1u : 0u) + ((lo <= v[q]) && (v[q] < t) ? 0x10000u : 0u);
         const unsigned excl = warp_incl_scan(packed) - packed;
         int ea = (int)(excl & 0xffffu), eb = (int)(excl >> 16);
         const int i0 = lane * E;
 #pragma unroll
         for (int q = 0; q < E; ++q) {
-            if (pa[q]) {
+            if (v[q] >= t) {
                 const int pos = ea + min(eb, need);
                 if (pos < k) stage_put(sbase + 8u * pos, v[q], i0 + q);
                 ++ea;
-            } else if (pb[q]) {
+            } else if (lo <= v[q]) {
                 if (eb < need && ea + eb < k) stage_put(sbase + 8u * (ea + eb), v[q], i0 + q);
                 ++eb;
             }

@@ -167,8 +167,8 @@ def _mixed_rows(rng, n, m):
     return np.stack(rows)
 
 
-@pytest.mark.parametrize("m", [4, 8, 100, 128, 200, 256, 260, 384, 500, 512, 640, 768, 1000, 1024, 1028, 2048, 3000,
-                               4096, 8192])
+@pytest.mark.parametrize("m", [4, 8, 100, 128, 200, 256, 260, 384, 500, 512, 640, 768, 1000, 1024, 1025, 1028, 1536,
+                               1537, 2048, 2049, 3000, 3072, 3073, 4096, 4097, 6144, 6145, 8192])
 def test_fast_paths_mixed_rows_vs_oracle(oracle_lib, m):
     """The no-trace hot paths (paired-row kernel for M <= 256, long-row kernel
     above, masked and unmasked tiles) on odd row counts mixing fast-loop rows
@@ -198,7 +198,8 @@ def test_fast_paths_many_grid_steps_vs_oracle(oracle_lib):
     the oracle."""
     g = torch.Generator(device="cuda").manual_seed(11)
     for n, m, k in ((300_001, 256, 32), (300_001, 128, 16), (120_001, 1024, 64), (150_001, 512, 64),
-                    (100_003, 768, 128), (20_001, 2048, 64), (9_001, 8192, 256)):
+                    (100_003, 768, 128), (20_001, 2048, 64), (30_001, 1500, 64), (12_001, 3072, 128),
+                    (10_001, 4000, 64), (9_001, 5000, 64), (9_001, 8192, 256)):
         x = torch.randn(n, m, device="cuda", generator=g)
         rows = torch.tensor([0, 1, 2, 3, n // 3, n // 2 + 1, n - 4, n - 3, n - 2, n - 1], device="cuda")
         xs = x[rows].cpu().numpy()
@@ -393,3 +394,22 @@ def test_input_dtypes_convert_like_as_matrix(oracle_lib):
             ctx = (type(x).__name__, getattr(x, "dtype", None), mode)
             assert np.array_equal(_np(res.indices), want[1]), ctx
             assert np.array_equal(_bits(_np(res.values)), _bits(want[0])), ctx
+
+
+def test_long_rows_large_k_shared_memory_fits(oracle_lib):
+    """Long rows with k close to M need 8k bytes of staging per warp: the
+    launch shrinks the CTA to fit shared memory.  Launches alternate between
+    large and small staging on the same kernels (the opt-in size must never
+    shrink under a cached launch)."""
+    rng = np.random.default_rng(31)
+    for m in (1500, 2048, 3000, 4096, 6000, 8192):
+        x = rng.standard_normal((37, m), dtype=np.float32)
+        for k in (m - 1, 3, m // 2, m):
+            for mode in ("exact", "early"):
+                want = oracle_lib.ref_batch(x, k, mode, max_iter=4)
+                for traces in (True, False):
+                    res = rtk.batch_topk(torch.from_numpy(x).cuda(),
+                                         rtk.BatchConfig(k=k, search=_search(mode, 4), collect_traces=traces))
+                    ctx = (m, k, mode, traces)
+                    assert np.array_equal(_np(res.indices), want[1]), ctx
+                    assert np.array_equal(_bits(_np(res.values)), _bits(want[0])), ctx

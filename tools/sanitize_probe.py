@@ -16,8 +16,8 @@ import paper_2409_00822_b200 as rtk  # noqa: E402
 
 def main():
     rng = np.random.default_rng(0)
-    for m in (4, 8, 100, 128, 256, 257, 384, 512, 777, 1024, 1500):
-        n = 67
+    for m in (4, 8, 100, 128, 256, 257, 384, 512, 777, 1024, 1500, 2048, 2500, 3072, 4000, 4500, 6144, 8192):
+        n = 67 if m <= 1024 else 19
         x = rng.standard_normal((n, m), dtype=np.float32)
         x[5] = 1.0
         x[9, : m // 2] = np.inf
@@ -29,7 +29,7 @@ def main():
                     assert np.array_equal(res.indices.cpu().numpy(), i), (m, k, mode, traces)
                     assert np.array_equal(res.values.cpu().numpy().view(np.uint32), v.view(np.uint32)), (m, k, mode)
         xn = x.copy()
-        xn[40, m - 1] = np.nan
+        xn[n - 3, m - 1] = np.nan
         try:
             rtk.batch_topk(xn, rtk.BatchConfig(k=1))
             raise AssertionError("NaN not reported")
