@@ -23,9 +23,12 @@ run_full c2_early early
 run_full m1024_exact exact 1048576:1024:64
 run_full m1024_early early 1048576:1024:64
 run_full m512_early early 1048576:512:64
-run_full m4096_exact exact 262144:4096:64
+run_full m2048_exact exact 524288:2048:64
+run_full m2048_early early 524288:2048:64
+run_full m8192_exact exact 131072:8192:128
 timeout 900 python tools/sweep_bench.py --out $OUT/sweep.json > $OUT/sweep.log 2>&1
 timeout 600 python tools/maxk_bench.py > $OUT/maxk_bench.json 2> $OUT/maxk_bench.err
+timeout 900 python tools/sweep_bench.py --shapes "1100:32,1536:64,2048:64,2500:64,3072:128,4000:64,4096:128,4500:64,6144:128,8192:128" --no-extra --no-torch --steps 30 > $OUT/sweep_long.log 2>&1
 timeout 600 python tools/file_bench.py /dev/shm > $OUT/file_bench_tmpfs.json 2> $OUT/file_bench.err
 timeout 300 python tools/pcie_probe.py > $OUT/pcie_probe.json 2>&1
 timeout 900 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log

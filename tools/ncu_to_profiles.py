@@ -22,7 +22,9 @@ CAPTURES = {  # capture -> (bench workload key, rows)
     "m1024_exact": ("custom 1048576:1024:64:exact", 1 << 20),
     "m1024_early": ("custom 1048576:1024:64:early", 1 << 20),
     "m512_early": ("custom 1048576:512:64:early", 1 << 20),
-    "m4096_exact": ("custom 262144:4096:64:exact", 1 << 18),
+    "m2048_exact": ("custom 524288:2048:64:exact", 1 << 19),
+    "m2048_early": ("custom 524288:2048:64:early", 1 << 19),
+    "m8192_exact": ("custom 131072:8192:128:exact", 1 << 17),
 }
 RAW_KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
             "sm__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__issue_active.avg.pct_of_peak_sustained_active",
