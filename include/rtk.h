@@ -143,9 +143,14 @@ RTK_API const char *rtk_last_error(void);
 /* Library ABI version (major*10000 + minor*100 + patch). */
 RTK_API int rtk_version(void);
 
-/* Device-side tuning knobs the host wrapper may report: the warps per CTA and
- * CTAs per SM the persistent kernels launch with for (m, k, mode); mode 0 =
- * exact, 1 = early stop, 2 = trace.  Returns RTK_OK or RTK_EINVAL. */
+/* The launch configuration the dispatcher picks for an aligned, contiguous
+ * 2^20 x m matrix (no traces for modes 0/1; mode 0 = exact, 1 = early stop,
+ * 2 = trace) on the current device, without launching: warps per CTA,
+ * resident CTAs per SM (occupancy of that kernel instantiation; 1 when no
+ * device is present) and rows a warp works on at a time (2 = paired-row
+ * kernel, 1 = one row per warp, 0 = the CTA's warps share one row).  For
+ * k == m: the elementwise copy (8 warps, 0, 0).  Returns RTK_OK or
+ * RTK_EINVAL. */
 RTK_API int rtk_launch_shape(int64_t m, int32_t k, int32_t mode, int32_t *warps_per_cta,
                      int32_t *ctas_per_sm, int32_t *rows_per_warp);
 

@@ -279,11 +279,26 @@ int rtk_version(void) { return 100; }
 
 int rtk_launch_shape(int64_t m, int32_t k, int32_t mode, int32_t* warps_per_cta, int32_t* ctas_per_sm_out,
                      int32_t* rows_per_warp) {
-    if (m < 1 || k < 1 || k > m || mode < 0 || mode > 2) return fail(RTK_EINVAL, "bad launch-shape query");
-    if (warps_per_cta) *warps_per_cta = rtk_dispatch::kThreads / 32;
-    if (ctas_per_sm_out) *ctas_per_sm_out = 0;  // resolved per instantiation at launch
-    if (rows_per_warp) *rows_per_warp = 1;
-    return RTK_OK;
+    if (m < 1 || m > 0x7fffffff || k < 1 || k > m || mode < 0 || mode > 2)
+        return fail(RTK_EINVAL, "bad launch-shape query");
+    // a 2^20-row, C-contiguous, 256-byte aligned matrix without traces (modes 0/1)
+    alignas(256) static const float kDummy[64] = {};
+    rtk::Args a = make_args(kDummy, 1 << 20, m, m, k, mode == rtk::kTrace ? nullptr : reinterpret_cast<float*>(256),
+                            mode == rtk::kTrace ? nullptr : reinterpret_cast<int32_t*>(256), k,
+                            mode == rtk::kTrace ? reinterpret_cast<int32_t*>(256) : nullptr,
+                            mode == rtk::kTrace ? reinterpret_cast<int8_t*>(256) : nullptr, nullptr);
+    int shape[3] = {0, 0, 0};
+    int rc = RTK_OK;
+    if (k == m) {
+        shape[0] = kFlatThreads / 32;  // elementwise copy (_kernels.py:173-179)
+    } else {
+        rc = mode == rtk::kExact ? rtk_describe_exact(a, shape)
+                                 : (mode == rtk::kEarly ? rtk_describe_early(a, shape) : rtk_describe_trace(a, shape));
+    }
+    if (warps_per_cta) *warps_per_cta = shape[0];
+    if (ctas_per_sm_out) *ctas_per_sm_out = shape[1];
+    if (rows_per_warp) *rows_per_warp = shape[2];
+    return rc;
 }
 
 }  // extern "C"

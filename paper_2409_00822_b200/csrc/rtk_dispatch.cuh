@@ -22,6 +22,9 @@ int rtk_ctas_per_sm(const void* kernel, size_t smem, int threads);
 int rtk_dispatch_exact(const rtk::Args& a, cudaStream_t s);
 int rtk_dispatch_early(const rtk::Args& a, cudaStream_t s);
 int rtk_dispatch_trace(const rtk::Args& a, cudaStream_t s);
+int rtk_describe_exact(const rtk::Args& a, int* shape3);
+int rtk_describe_early(const rtk::Args& a, int* shape3);
+int rtk_describe_trace(const rtk::Args& a, int* shape3);
 bool rtk_encode_row_map(CUtensorMap* map, const float* x, long long n, int e, long long ldx);
 
 namespace rtk_dispatch {
@@ -42,8 +45,25 @@ constexpr int kFlatThreads = 256;         // threads per CTA of the elementwise 
 constexpr size_t kMaxSmem = 227 * 1024;   // dynamic shared memory per CTA (sm_100 opt-in limit)
 
 
+// Dry-run description of a launch (rtk_launch_shape): when set, the launch
+// helpers record the chosen configuration here instead of launching.
+struct LaunchShape {
+    int warps_per_cta, ctas_per_sm, rows_per_warp;
+};
+inline thread_local LaunchShape* g_describe = nullptr;
+
+inline bool describe(const void* kernel, size_t smem, int threads, int rows_per_warp) {
+    if (!g_describe) return false;
+    g_describe->warps_per_cta = threads / 32;
+    g_describe->ctas_per_sm = rtk_ctas_per_sm(kernel, smem, threads);
+    g_describe->rows_per_warp = rows_per_warp;
+    return true;
+}
+
 template <class K>
-int launch_rows(K kernel, const rtk::Args& a, cudaStream_t s, size_t smem, int threads = kThreads) {
+int launch_rows(K kernel, const rtk::Args& a, cudaStream_t s, size_t smem, int threads = kThreads,
+                int rows_per_warp = 1) {
+    if (describe(reinterpret_cast<const void*>(kernel), smem, threads, rows_per_warp)) return RTK_OK;
     const long long warps_needed = a.n;
     const long long blocks_needed = (warps_needed + (threads / 32) - 1) / (threads / 32);
     long long grid = (long long)rtk_device_sms() * rtk_ctas_per_sm(reinterpret_cast<const void*>(kernel), smem, threads);
@@ -101,6 +121,7 @@ int launch_big_tma_kernel(const rtk::Args& a, cudaStream_t s, const CUtensorMap&
     constexpr int wpc = RTK_BIG_THREADS / 32;
     const size_t smem = (size_t)wpc * Row::stage_bytes(a.k) + Row::kSlotAlign + (size_t)wpc * (Row::kSlotBytes + 8);
     auto kernel = rtk::rowtopk_big_tma_kernel<MODE, E, TRACES>;
+    if (describe(reinterpret_cast<const void*>(kernel), smem, RTK_BIG_THREADS, 1)) return RTK_OK;
     const long long blocks_needed = (a.n + wpc - 1) / wpc;
     long long grid = (long long)rtk_device_sms() * rtk_ctas_per_sm(reinterpret_cast<const void*>(kernel), smem,
                                                                    RTK_BIG_THREADS);
@@ -158,9 +179,10 @@ int launch_pair(const rtk::Args& a, cudaStream_t s) {
         // two selection staging buffers per warp
         const size_t smem = (size_t)(kThreads / 32) * 2 * rtk::LaneRow<E, false>::kStageBytes;
         const bool wide = (reinterpret_cast<uintptr_t>(a.x) & 31) == 0 && a.ldx % 8 == 0;  // 256-bit loads
-        if (a.m == 32 * E && wide) return launch_rows(rtk::rowtopk_pair_kernel<MODE, E, false, true>, a, s, smem);
-        if (a.m == 32 * E) return launch_rows(rtk::rowtopk_pair_kernel<MODE, E, false, false>, a, s, smem);
-        return launch_rows(rtk::rowtopk_pair_kernel<MODE, E, true, false>, a, s, smem);
+        if (a.m == 32 * E && wide)
+            return launch_rows(rtk::rowtopk_pair_kernel<MODE, E, false, true>, a, s, smem, kThreads, 2);
+        if (a.m == 32 * E) return launch_rows(rtk::rowtopk_pair_kernel<MODE, E, false, false>, a, s, smem, kThreads, 2);
+        return launch_rows(rtk::rowtopk_pair_kernel<MODE, E, true, false>, a, s, smem, kThreads, 2);
     }
 }
 
@@ -197,6 +219,7 @@ int launch_block_kernel(const rtk::Args& a, cudaStream_t s) {
     const int threads = W * 32;
     const size_t smem = (((size_t)8 * a.k + 15) & ~(size_t)15) + (size_t)W * Tile::kRowBytes;
     auto kernel = rtk::rowtopk_block_kernel<MODE, W, E, TRACES>;
+    if (describe(reinterpret_cast<const void*>(kernel), smem, threads, 0)) return RTK_OK;  // W warps per row
     long long grid = (long long)rtk_device_sms() * rtk_ctas_per_sm(reinterpret_cast<const void*>(kernel), smem, threads);
     if (grid > a.n) grid = a.n;
     if (grid < 1) grid = 1;
@@ -269,5 +292,18 @@ int dispatch(const rtk::Args& a, cudaStream_t s) {
 #endif
 }
 
+
+// The configuration dispatch<MODE> would launch for `a` (no launch).
+template <int MODE>
+int describe_dispatch(const rtk::Args& a, int* shape3) {
+    LaunchShape sh{0, 0, 0};
+    g_describe = &sh;
+    const int rc = dispatch<MODE>(a, nullptr);
+    g_describe = nullptr;
+    shape3[0] = sh.warps_per_cta;
+    shape3[1] = sh.ctas_per_sm;
+    shape3[2] = sh.rows_per_warp;
+    return rc;
+}
 
 }  // namespace rtk_dispatch

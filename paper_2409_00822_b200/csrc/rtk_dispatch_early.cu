@@ -2,3 +2,4 @@
 #include "rtk_dispatch.cuh"
 
 int rtk_dispatch_early(const rtk::Args& a, cudaStream_t s) { return rtk_dispatch::dispatch<rtk::kEarly>(a, s); }
+int rtk_describe_early(const rtk::Args& a, int* shape3) { return rtk_dispatch::describe_dispatch<rtk::kEarly>(a, shape3); }

@@ -413,3 +413,24 @@ def test_long_rows_large_k_shared_memory_fits(oracle_lib):
                     ctx = (m, k, mode, traces)
                     assert np.array_equal(_np(res.indices), want[1]), ctx
                     assert np.array_equal(_bits(_np(res.values)), _bits(want[0])), ctx
+
+
+def test_launch_shape_describes_the_dispatch():
+    """rtk_launch_shape reports the kernel family the dispatcher picks."""
+    import ctypes
+
+    lib = rtk._native.load()
+
+    def shape(m, k, mode):
+        w, c, r = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        assert lib.rtk_launch_shape(m, k, mode, ctypes.byref(w), ctypes.byref(c), ctypes.byref(r)) == 0
+        return w.value, c.value, r.value
+
+    assert shape(256, 32, 0)[2] == 2 and shape(128, 16, 1)[2] == 2      # paired rows
+    assert shape(256, 32, 2)[2] == 1                                      # traces: one row per warp
+    for m in (512, 1024, 2048, 4096):
+        w, c, r = shape(m, 64, 0)
+        assert r == 1 and w >= 1 and c >= 1, (m, w, c, r)
+    assert shape(8192, 64, 0)[::2] == (2, 0) and shape(8192, 64, 1)[::2] == (4, 0)  # CTA per row
+    assert shape(3000, 2999, 1)[0] < 8                                    # large k: fewer warps per CTA
+    assert shape(128, 128, 0) == (8, 0, 0)                                # k == M copy
