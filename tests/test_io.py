@@ -152,3 +152,35 @@ def test_matrix_roundtrip_bytes(gpu, tmp_path):
     _write_rtkm(q, bad)
     with pytest.raises(rtk.NaNInputError):
         rtk.load_matrix(q)
+
+
+def test_cli_parser(tmp_path):
+    """CLI arguments mirror the reference's `run` / `gen` (cli.py:53-72);
+    failures map to the reference's exit codes."""
+    from paper_2409_00822_b200 import cli
+
+    a = cli.build_parser().parse_args(["run", "--matrix", "m", "--k", "3", "--out", "o", "--mode", "early-stop"])
+    assert (a.k, a.mode, a.max_iter, a.hard_cap, a.workers, a.epsilon_rel) == (3, "early-stop", 4, 64, "auto", 0.0)
+    assert cli.build_parser().parse_args(["gen", "--rows", "5", "--cols", "7", "--out", "o"]).seed == 0
+    bad = tmp_path / "bad.rtkm"
+    bad.write_bytes(b"NOPE" + bytes(20))
+    assert cli.main(["run", "--matrix", str(bad), "--k", "1", "--out", str(tmp_path / "o")]) in (1, 3)
+
+
+@pytest.mark.gpu
+def test_cli_run_matches_batch_topk(tmp_path):
+    """`run` output bytes == save_result(batch_topk(load_matrix(...))); error
+    exit codes as the reference's (3 i/o, 1 validation)."""
+    from paper_2409_00822_b200 import cli
+
+    p, out, ref = tmp_path / "x.rtkm", tmp_path / "r.rtkr", tmp_path / "ref.rtkr"
+    assert cli.main(["gen", "--rows", "5", "--cols", "7", "--seed", "3", "--out", str(p)]) == 0
+    np.testing.assert_array_equal(rtk.load_matrix(p), rtk.generate_matrix(rtk.DataGenSpec(5, 7, seed=3)))
+    assert cli.main(["gen", "--rows", "3001", "--cols", "256", "--out", str(p)]) == 0
+    for mode in (["--mode", "exact"], ["--mode", "early-stop", "--max-iter", "3"]):
+        assert cli.main(["run", "--matrix", str(p), "--k", "32", "--out", str(out), *mode]) == 0
+        search = rtk.SearchConfig.exact() if mode[1] == "exact" else rtk.SearchConfig.early_stop(3)
+        rtk.save_result(rtk.batch_topk(rtk.load_matrix(p), rtk.BatchConfig(k=32, search=search)), ref)
+        assert out.read_bytes() == ref.read_bytes()
+    assert cli.main(["run", "--matrix", str(tmp_path / "missing"), "--k", "1", "--out", str(out)]) == 3
+    assert cli.main(["run", "--matrix", str(p), "--k", "999", "--out", str(out)]) == 1
