@@ -55,6 +55,7 @@ extern "C" {
 #define RTK_EFORMAT 4 /* bad magic or unsupported format version */
 #define RTK_ETRUNC 5  /* file shorter than its header declares, or empty payload */
 #define RTK_ENAN 6    /* the matrix holds a NaN (first offending row reported) */
+#define RTK_EUNSUPPORTED 7 /* rtk_rowtopk_x16: shape/layout outside its native path */
 
 #define RTK_EXIT_COUNT_EQUALS_K 1
 #define RTK_EXIT_INTERVAL_BELOW_EPSILON 2
@@ -81,6 +82,19 @@ RTK_API int rtk_rowtopk_early_f32(const float *x, int64_t n, int64_t m, int64_t 
                           int32_t max_iter, float *vals, int32_t *idx, int64_t ldo,
                           int32_t *iters, int8_t *reasons, uint32_t *nan_first_row,
                           void *stream);
+
+/* Row top-k of a 16-bit float matrix read natively (dtype 1 = bfloat16,
+ * 2 = float16) and widened to float32 in registers.  The widening is exact,
+ * so the outputs (float32 values, int32 indices) equal rtk_rowtopk_*_f32 on
+ * the float32 image of x -- which is what the reference computes, since
+ * as_matrix converts every input to float32 (batch.py:30-36) -- with half
+ * the input bytes and no conversion pass.  mode 0 = exact (eps_rel = 0,
+ * hard_cap), 1 = early stop (max_iter); no traces.  Native path: 1 <= k < m,
+ * m <= 256, m % 4 == 0, ldx % 4 == 0, x 8-byte aligned; anything else
+ * returns RTK_EUNSUPPORTED (convert to float32 and use the _f32 calls). */
+RTK_API int rtk_rowtopk_x16(const void *x, int32_t dtype, int32_t mode, int64_t n, int64_t m, int64_t ldx,
+                    int32_t k, int32_t hard_cap, int32_t max_iter, float *vals, int32_t *idx,
+                    int64_t ldo, uint32_t *nan_first_row, void *stream);
 
 /* Exit statistics only, no selection.  Replaces
  *   _kernels.exact_trace_chunk(data, k, eps_rel, hard_cap, out_iters, out_reasons)

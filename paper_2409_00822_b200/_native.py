@@ -13,7 +13,7 @@ import threading
 from ._build import SO
 from .errors import DeviceError
 
-RTK_OK, RTK_EINVAL, RTK_ECUDA, RTK_EIO, RTK_EFORMAT, RTK_ETRUNC, RTK_ENAN = 0, 1, 2, 3, 4, 5, 6
+RTK_OK, RTK_EINVAL, RTK_ECUDA, RTK_EIO, RTK_EFORMAT, RTK_ETRUNC, RTK_ENAN, RTK_EUNSUPPORTED = 0, 1, 2, 3, 4, 5, 6, 7
 
 _lock = threading.Lock()
 _lib = None
@@ -30,6 +30,7 @@ SIGNATURES = {
                                              _p, _p, _i64, _p, _p, _p, _p]),
     "rtk_exact_trace_f32": (ctypes.c_int, [_p, _i64, _i64, _i64, _i32, ctypes.c_double, _i32,
                                            _p, _p, _p, _p]),
+    "rtk_rowtopk_x16": (ctypes.c_int, [_p, _i32, _i32, _i64, _i64, _i64, _i32, _i32, _i32, _p, _p, _i64, _p, _p]),
     "rtk_nan_scan_f32": (ctypes.c_int, [_p, _i64, _i64, _i64, _p, _p]),
     "rtk_row_min_max_f32": (ctypes.c_int, [_p, _i64, _i64, _i64, _p, _p, _p]),
     "rtk_count_ge_f32": (ctypes.c_int, [_p, _i64, _i64, _i64, _p, _p, _p]),

@@ -79,6 +79,8 @@ class _DeviceMatrix:
 
     def __init__(self, values):
         torch = _require_cuda()
+        self._x = None
+        self.x16 = None
         self.host = not (_is_torch(values) and values.is_cuda)
         if self.host:
             if _is_torch(values) and values.dim() == 2 and values.dtype == torch.float32:
@@ -89,22 +91,40 @@ class _DeviceMatrix:
                 with warnings.catch_warnings():  # read-only arrays (memmaps) are only read from
                     warnings.simplefilter("ignore", UserWarning)
                     t = torch.from_numpy(_host_matrix(values))
-            self.x = t.to(torch.device("cuda", torch.cuda.current_device()),
-                          non_blocking=t.is_pinned())
+            self._x = t.to(torch.device("cuda", torch.cuda.current_device()),
+                           non_blocking=t.is_pinned())
         else:
             t = values
             if t.dim() != 2:
                 raise DimensionMismatchError(f"expected a 2-D matrix, got shape {tuple(t.shape)}")
             if t.shape[0] == 0 or t.shape[1] == 0:
                 raise EmptyRowError(f"matrix must be at least 1 x 1, got {tuple(t.shape)}")
-            if t.dtype != torch.float32:
-                t = t.to(torch.float32)
-            if t.stride(1) != 1 or (t.shape[0] > 1 and t.stride(0) < t.shape[1]):
-                t = t.contiguous()
-            self.x = t
-        self.n, self.m = int(self.x.shape[0]), int(self.x.shape[1])
-        self.ldx = int(self.x.stride(0)) if self.n > 1 else self.m
-        self.device = self.x.device
+            if t.dtype in (torch.bfloat16, torch.float16) and t.stride(1) == 1 and (
+                    t.shape[0] == 1 or t.stride(0) >= t.shape[1]):
+                # kept as is: the top-k launch reads 16-bit rows natively where
+                # it can (rtk_rowtopk_x16); other uses widen on first access
+                self.x16 = t
+            else:
+                if t.dtype != torch.float32:
+                    t = t.to(torch.float32)
+                if t.stride(1) != 1 or (t.shape[0] > 1 and t.stride(0) < t.shape[1]):
+                    t = t.contiguous()
+                self._x = t
+        src = self._x if self._x is not None else self.x16
+        self.n, self.m = int(src.shape[0]), int(src.shape[1])
+        self.device = src.device
+
+    @property
+    def x(self):
+        """The matrix as float32 on the device (16-bit inputs are widened --
+        exactly -- on first use, as as_matrix does, batch.py:30-36)."""
+        if self._x is None:
+            self._x = self.x16.to(_torch().float32).contiguous()
+        return self._x
+
+    @property
+    def ldx(self) -> int:
+        return int(self.x.stride(0)) if self.n > 1 else self.m
 
     # -- plumbing
     def _stream(self):
@@ -163,6 +183,19 @@ class _DeviceMatrix:
         it_p = iters.data_ptr() if iters is not None else None
         rs_p = reasons.data_ptr() if reasons is not None else None
         nan_p = nan_word.data_ptr() if nan_word is not None else None
+        ldo = int(vals.stride(0)) if self.n > 1 else int(k)
+        if self.x16 is not None and not traces and (search.mode is SearchMode.EARLY_STOP or
+                                                    search.epsilon_rel == 0.0):
+            dtype = 1 if self.x16.dtype == torch.bfloat16 else 2
+            mode = 0 if search.mode is SearchMode.EXACT else 1
+            ldx16 = int(self.x16.stride(0)) if self.n > 1 else self.m
+            with torch.cuda.device(self.device):
+                rc = _native.load().rtk_rowtopk_x16(self.x16.data_ptr(), dtype, mode, self.n, self.m, ldx16, int(k),
+                                                    int(search.hard_cap), int(search.max_iter), vals.data_ptr(),
+                                                    idx.data_ptr(), ldo, nan_p, s)
+            if rc != _native.RTK_EUNSUPPORTED:
+                _native.check(rc, "rtk_rowtopk_x16")
+                return vals, idx, iters, reasons
         with torch.cuda.device(self.device):
             if search.mode is SearchMode.EXACT:
                 _native.call("rtk_rowtopk_exact_f32", self.x.data_ptr(), self.n, self.m, self.ldx, int(k),
@@ -417,8 +450,10 @@ def batch_topk(matrix, cfg: BatchConfig) -> BatchResult:
 
 
 def topk_device(x, k: int, search: SearchConfig | None = None, nan_word=None):
-    """Row top-k of a CUDA float32 matrix enqueued on the current stream with
-    no host synchronisation (capturable in a CUDA graph): returns device
+    """Row top-k of a CUDA matrix (float32; bfloat16 / float16 rows of up to
+    256 columns are read natively, others widened) enqueued on the current
+    stream with no host synchronisation (capturable in a CUDA graph; the
+    16-bit widening of unsupported shapes allocates): returns device
     (values, indices).  NaN rows are not raised here -- pass a 1-element
     int32 CUDA tensor as `nan_word` to receive the first offending row
     (-1 when none) and check it when convenient.  Validation of shape and k

@@ -225,6 +225,33 @@ int rtk_rowtopk_early_f32(const float* x, int64_t n, int64_t m, int64_t ldx, int
                           nan_first_row, stream);
 }
 
+int rtk_rowtopk_x16(const void* x, int32_t dtype, int32_t mode, int64_t n, int64_t m, int64_t ldx, int32_t k,
+                    int32_t hard_cap, int32_t max_iter, float* vals, int32_t* idx, int64_t ldo,
+                    uint32_t* nan_first_row, void* stream) {
+    if (dtype != 1 && dtype != 2) return fail(RTK_EINVAL, "dtype must be 1 (bfloat16) or 2 (float16), got %d", dtype);
+    if (mode != rtk::kExact && mode != rtk::kEarly) return fail(RTK_EINVAL, "mode must be 0 or 1, got %d", mode);
+    int rc = check_common(static_cast<const float*>(x), n, m, ldx);
+    if (rc) return rc;
+    if (k < 1 || k > m) return fail(RTK_EINVAL, "k must be in [1, %lld], got %d", (long long)m, k);
+    if (ldo < k) return fail(RTK_EINVAL, "ldo (%lld) < k (%d)", (long long)ldo, k);
+    if (ldo >= (1LL << 30)) return fail(RTK_EINVAL, "ldo must be < 2^30, got %lld", (long long)ldo);
+    if (n > 0 && (!vals || !idx)) return fail(RTK_EINVAL, "vals/idx is NULL");
+    if (mode == rtk::kExact && hard_cap < 1) return fail(RTK_EINVAL, "hard_cap must be >= 1, got %d", hard_cap);
+    if (mode == rtk::kEarly && max_iter < 1) return fail(RTK_EINVAL, "max_iter must be >= 1, got %d", max_iter);
+    if (k == m || m > 256 || m % 4 != 0 || ldx % 4 != 0 || (reinterpret_cast<uintptr_t>(x) & 7) != 0 ||
+        n >= 0xffff0000LL)
+        return fail(RTK_EUNSUPPORTED, "shape outside the native 16-bit path (m=%lld, k=%d, ldx=%lld)",
+                    (long long)m, k, (long long)ldx);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    rc = reset_nan(nan_first_row, s);
+    if (rc || n == 0) return rc;
+    rtk::Args a = make_args(static_cast<const float*>(x), n, m, ldx, k, vals, idx, ldo, nullptr, nullptr,
+                            nan_first_row);
+    a.hard_cap = hard_cap;
+    a.max_iter = max_iter;
+    return rtk_dispatch_x16(a, dtype, mode, s);
+}
+
 int rtk_exact_trace_f32(const float* x, int64_t n, int64_t m, int64_t ldx, int32_t k, double eps_rel,
                         int32_t hard_cap, int32_t* iters, int8_t* reasons, uint32_t* nan_first_row, void* stream) {
     return rowtopk_common(rtk::kTrace, x, n, m, ldx, k, eps_rel, hard_cap, 1, nullptr, nullptr, k, iters, reasons,

@@ -20,8 +20,12 @@
 //   * compiled without fast-math, -ftz=false, -fmad=false.
 #pragma once
 
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <type_traits>
 
 namespace rtk {
 
@@ -383,6 +387,44 @@ struct LaneRow {
                 } else {
                     v[4 * g] = v[4 * g + 1] = v[4 * g + 2] = v[4 * g + 3] = __int_as_float(0x7fffffff);
                 }
+            }
+        }
+    }
+
+    // 16-bit rows (In = __nv_bfloat16 / __half), widened to fp32 exactly:
+    // one 16-byte load per lane (WIDE: E = 8, unmasked, 16-byte aligned rows)
+    // or 8-byte loads per 4 slots; padding slots hold NaN.
+    template <class In>
+    __device__ __forceinline__ void load16(const In* __restrict__ p, int m, int lane) {
+        const In* lp = p + lane * E;
+        unsigned w[E / 2];
+        if constexpr (WIDE && !MASKED && E % 8 == 0) {
+#pragma unroll
+            for (int g = 0; g < E / 8; ++g)
+                asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(w[4 * g]), "=r"(w[4 * g + 1]), "=r"(w[4 * g + 2]), "=r"(w[4 * g + 3])
+                             : "l"(lp + 8 * g));
+        } else {
+#pragma unroll
+            for (int g = 0; g < E / 4; ++g) {
+                if (valid(lane, 4 * g, m)) {
+                    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+                                 : "=r"(w[2 * g]), "=r"(w[2 * g + 1])
+                                 : "l"(lp + 4 * g));
+                } else {
+                    w[2 * g] = w[2 * g + 1] = 0xffffffffu;  // NaN in both formats
+                }
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < E / 2; ++h) {
+            if constexpr (std::is_same<In, __nv_bfloat16>::value) {
+                v[2 * h] = __uint_as_float(w[h] << 16);
+                v[2 * h + 1] = __uint_as_float(w[h] & 0xffff0000u);
+            } else {
+                const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[h]));
+                v[2 * h] = f.x;
+                v[2 * h + 1] = f.y;
             }
         }
     }

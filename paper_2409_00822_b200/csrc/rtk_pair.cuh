@@ -201,10 +201,20 @@ __device__ __forceinline__ void process_pair(const Row& A, const Row& B, unsigne
     }
 }
 
+// Row r of the input into a register tile: fp32 rows as they are, 16-bit
+// rows (In = __nv_bfloat16 / __half, rtk_rowtopk_x16) widened on load.
+template <class In, class Row>
+__device__ __forceinline__ void load_tile(Row& R, const Args& a, unsigned r, unsigned ldx_b, int lane) {
+    if constexpr (std::is_same<In, float>::value)
+        R.load(row_ptr(a.x, r, ldx_b), a.m, lane);
+    else
+        R.template load16<In>(row_ptr(reinterpret_cast<const In*>(a.x), r, ldx_b), a.m, lane);
+}
+
 // Persistent loop over row pairs (r, r + nw), stepping 2 nw; register
 // double buffering of the pair (the roles of the two tile pairs alternate
-// between the two unrolled halves).
-template <int MODE, int E, bool MASKED, bool WIDE>
+// between the two unrolled halves).  In: the input element type.
+template <int MODE, int E, bool MASKED, bool WIDE, class In = float>
 __global__ void __launch_bounds__(RTK_CTA_THREADS, PairMinCtas<E>::value) rowtopk_pair_kernel(Args a) {
     using Row = LaneRow<E, MASKED, WIDE>;
     extern __shared__ __align__(16) float smem[];
@@ -218,26 +228,26 @@ __global__ void __launch_bounds__(RTK_CTA_THREADS, PairMinCtas<E>::value) rowtop
     unsigned r = blockIdx.x * wpc + (unsigned)wid;
     if (r >= n) return;
     const unsigned last = n - 1;
-    const unsigned ldx_b = (unsigned)a.ldx * 4u;
+    const unsigned ldx_b = (unsigned)a.ldx * (unsigned)sizeof(In);
     const unsigned oz = a.opaque_zero;
     const int steps = MODE == kEarly ? a.max_iter : min(a.hard_cap, RTK_FAST_STEPS);
     Row A, B, C, D;
-    A.load(row_ptr(a.x, r, ldx_b), a.m, lane);
-    B.load(row_ptr(a.x, min(r + nw, last), ldx_b), a.m, lane);
+    load_tile<In>(A, a, r, ldx_b, lane);
+    load_tile<In>(B, a, min(r + nw, last), ldx_b, lane);
     for (;;) {
         const unsigned rn = r + 2 * nw;
         process_pair<MODE>(A, B, r, r + nw, r + nw < n, a, lane, sA, sB, steps, [&](unsigned tok) {
             tok &= oz;
-            C.load(row_ptr(a.x, min(rn, last) + tok, ldx_b), a.m, lane);
-            D.load(row_ptr(a.x, min(rn + nw, last) + tok, ldx_b), a.m, lane);
+            load_tile<In>(C, a, min(rn, last) + tok, ldx_b, lane);
+            load_tile<In>(D, a, min(rn + nw, last) + tok, ldx_b, lane);
         });
         if (rn >= n) break;
         r = rn;
         const unsigned rn2 = r + 2 * nw;
         process_pair<MODE>(C, D, r, r + nw, r + nw < n, a, lane, sA, sB, steps, [&](unsigned tok) {
             tok &= oz;
-            A.load(row_ptr(a.x, min(rn2, last) + tok, ldx_b), a.m, lane);
-            B.load(row_ptr(a.x, min(rn2 + nw, last) + tok, ldx_b), a.m, lane);
+            load_tile<In>(A, a, min(rn2, last) + tok, ldx_b, lane);
+            load_tile<In>(B, a, min(rn2 + nw, last) + tok, ldx_b, lane);
         });
         if (rn2 >= n) break;
         r = rn2;

@@ -83,6 +83,7 @@ class _MaxK(torch.autograd.Function):
         values, indices = _select(x.detach(), k, search, check_nan)
         ctx.save_for_backward(indices)
         ctx.m = int(x.shape[1])
+        ctx.dtype = x.dtype
         ctx.mark_non_differentiable(indices)
         return values, indices
 
@@ -91,7 +92,7 @@ class _MaxK(torch.autograd.Function):
         (indices,) = ctx.saved_tensors
         if grad_values is None:
             return None, None, None, None
-        return scatter_rows(grad_values.contiguous(), indices, ctx.m), None, None, None
+        return scatter_rows(grad_values.contiguous(), indices, ctx.m).to(ctx.dtype), None, None, None
 
 
 class _MaxKDense(torch.autograd.Function):
@@ -99,17 +100,19 @@ class _MaxKDense(torch.autograd.Function):
     def forward(ctx, x, k, search, check_nan):
         values, indices = _select(x.detach(), k, search, check_nan)
         ctx.save_for_backward(indices)
-        return scatter_rows(values, indices, int(x.shape[1]))
+        return scatter_rows(values, indices, int(x.shape[1])).to(x.dtype)  # kept values are exact in x's dtype
 
     @staticmethod
     def backward(ctx, grad_out):
         (indices,) = ctx.saved_tensors
-        return scatter_rows(gather_rows(grad_out, indices), indices, int(grad_out.shape[1])), None, None, None
+        g = scatter_rows(gather_rows(grad_out, indices), indices, int(grad_out.shape[1]))
+        return g.to(grad_out.dtype), None, None, None
 
 
 def maxk(x: torch.Tensor, k: int, search: SearchConfig | None = None, check_nan: bool = True):
-    """Row top-k of a CUDA float32 matrix as (values, int32 indices); values
-    carry the gradient (scattered back to the selected columns).
+    """Row top-k of a CUDA matrix (float32, or bfloat16 / float16 read
+    natively for M <= 256) as (float32 values, int32 indices); values carry
+    the gradient (scattered back to the selected columns, in x's dtype).
     check_nan=False skips the NaN read-back (no host sync per call; the op
     can then be captured in a CUDA graph)."""
     return _MaxK.apply(x, int(k), search or SearchConfig.exact(), bool(check_nan))
@@ -117,7 +120,8 @@ def maxk(x: torch.Tensor, k: int, search: SearchConfig | None = None, check_nan:
 
 def maxk_dense(x: torch.Tensor, k: int, search: SearchConfig | None = None, check_nan: bool = True) -> torch.Tensor:
     """The MaxK nonlinearity in dense form: x with all but each row's top-k
-    entries set to zero (gradient flows to the kept entries only)."""
+    entries set to zero, in x's dtype (gradient flows to the kept entries
+    only)."""
     return _MaxKDense.apply(x, int(k), search or SearchConfig.exact(), bool(check_nan))
 
 

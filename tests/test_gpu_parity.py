@@ -434,3 +434,50 @@ def test_launch_shape_describes_the_dispatch():
     assert shape(8192, 64, 0)[::2] == (2, 0) and shape(8192, 64, 1)[::2] == (4, 0)  # CTA per row
     assert shape(3000, 2999, 1)[0] < 8                                    # large k: fewer warps per CTA
     assert shape(128, 128, 0) == (8, 0, 0)                                # k == M copy
+
+
+@pytest.mark.parametrize("dtype", ["bfloat16", "float16"])
+def test_16bit_rows_native_path(oracle_lib, dtype):
+    """bfloat16 / float16 CUDA matrices: M <= 256 rows are read natively by
+    rtk_rowtopk_x16 (paired-row kernel, widened in registers) and give the
+    oracle's result on the float32 image -- the reference's as_matrix
+    conversion; other shapes, traces and eps_rel > 0 widen on the device
+    first.  Covers masked/unmasked/16-byte/8-byte-aligned tiles, odd N,
+    strided views, NaN / inf / huge / tie-heavy rows."""
+    tdt = getattr(torch, dtype)
+    rng = np.random.default_rng(161)
+    for m in (4, 100, 128, 132, 200, 256, 300, 1024):
+        n = 1001
+        x = _mixed_rows(rng, n, m)
+        xd = torch.from_numpy(x).cuda().to(tdt)
+        x32 = xd.float().cpu().numpy()
+        for k in sorted({1, min(16, m - 1) or 1, max(1, m // 3), m - 1, m}):
+            for mode, mi, eps in (("exact", 4, 0.0), ("early", 3, 0.0), ("exact", 4, 1e-4)):
+                want = oracle_lib.ref_batch(x32, k, mode, max_iter=mi, eps_rel=eps)
+                for t in (xd, torch.nn.functional.pad(xd, (0, 8))[:, :m]):  # contiguous, strided (ldx = m + 8)
+                    for traces in (False, True):
+                        res = rtk.batch_topk(t, rtk.BatchConfig(k=k, search=_search(mode, mi, eps),
+                                                                collect_traces=traces))
+                        ctx = (dtype, m, k, mode, eps, traces, t.stride(0))
+                        assert res.values.dtype == torch.float32, ctx
+                        assert np.array_equal(_np(res.indices), want[1]), ctx
+                        assert np.array_equal(_bits(_np(res.values)), _bits(want[0])), ctx
+    bad = torch.randn(5000, 256, device="cuda").to(tdt)
+    bad[4321, 7] = float("nan")
+    with pytest.raises(rtk.NaNInputError, match="4321"):
+        rtk.batch_topk(bad, rtk.BatchConfig(k=8))
+    # the native entry point itself, and its refusal outside the native shape set
+    lib = rtk._native.load()
+    x = torch.randn(300_001, 256, device="cuda").to(tdt)
+    vals = torch.empty(300_001, 32, device="cuda")
+    idx = torch.empty(300_001, 32, dtype=torch.int32, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    code = 1 if dtype == "bfloat16" else 2
+    assert lib.rtk_rowtopk_x16(x.data_ptr(), code, 1, 300_001, 256, 256, 32, 64, 4, vals.data_ptr(), idx.data_ptr(),
+                               32, None, s) == 0
+    ref = rtk.batch_topk(x.float(), rtk.BatchConfig(k=32, search=rtk.SearchConfig.early_stop(4)))
+    assert torch.equal(vals, ref.values) and torch.equal(idx, ref.indices)
+    assert lib.rtk_rowtopk_x16(x.data_ptr(), code, 0, 10, 512, 512, 32, 64, 4, vals.data_ptr(), idx.data_ptr(),
+                               32, None, s) == 7  # RTK_EUNSUPPORTED: m > 256
+    assert lib.rtk_rowtopk_x16(x.data_ptr(), 3, 0, 10, 256, 256, 32, 64, 4, vals.data_ptr(), idx.data_ptr(),
+                               32, None, s) == 1  # bad dtype

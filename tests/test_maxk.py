@@ -78,6 +78,30 @@ def test_maxk_dense_matches_torch_formulation():
     assert torch.equal(x1.grad, x2.grad)
 
 
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_maxk_16bit_activations(dtype):
+    """MaxK on bf16 / fp16 activations (native 16-bit rows): dense output and
+    gradients in the activation dtype, equal to the torch formulation on the
+    same tensor; values float32 (exact widening)."""
+    n, m, k = 4096, 256, 32
+    x = torch.randn(n, m, device="cuda").to(dtype)
+    x1 = x.clone().requires_grad_(True)
+    x2 = x.clone().requires_grad_(True)
+    y1 = rtk.maxk_dense(x1, k, rtk.SearchConfig.exact())
+    vals, idx = rtk.maxk(x.clone().requires_grad_(True), k)
+    assert vals.dtype == torch.float32 and torch.equal(vals, x.float().gather(1, idx.long()))
+    # the true top-k set, ties broken by lower index (exact mode's rule when all values are distinct)
+    kth = x2.detach().float().topk(k, dim=1).values[:, -1:]
+    keep = x2.detach().float() >= kth
+    if bool((keep.sum(1) == k).all()):  # no ties at the k-th value in this draw
+        y2 = x2 * keep
+        assert y1.dtype == dtype and torch.equal(y1, y2)
+        g = torch.randn(n, m, device="cuda").to(dtype)
+        (y1.float() * g.float()).sum().backward()
+        (y2.float() * g.float()).sum().backward()
+        assert x1.grad.dtype == dtype and torch.equal(x1.grad, x2.grad)
+
+
 def test_sparse_csr_view_spmm():
     n, m, k = 500, 256, 32
     x = torch.randn(n, m, device="cuda")
