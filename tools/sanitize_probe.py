@@ -35,6 +35,14 @@ def main():
             raise AssertionError("NaN not reported")
         except rtk.NaNInputError:
             pass
+    for dt in (torch.bfloat16, torch.float16):  # native 16-bit rows (rtk_rowtopk_x16)
+        for m in (4, 100, 128, 132, 256):
+            xs = torch.randn(67, m, device="cuda").to(dt)
+            x32 = xs.float().cpu().numpy()
+            for search, mode, mi in ((rtk.SearchConfig.exact(), "exact", 4), (rtk.SearchConfig.early_stop(3), "early", 3)):
+                v, i, _, _ = oracle.ref_batch(x32, min(7, m - 1) or 1, mode, max_iter=mi)
+                res = rtk.batch_topk(xs, rtk.BatchConfig(k=min(7, m - 1) or 1, search=search))
+                assert np.array_equal(res.indices.cpu().numpy(), i), (dt, m, mode)
     xd = torch.randn(1000, 256, device="cuda")
     res = rtk.batch_topk(xd, rtk.BatchConfig(k=32))
     d = rtk.scatter_rows(res.values, res.indices, 256)
