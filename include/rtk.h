@@ -89,9 +89,10 @@ RTK_API int rtk_rowtopk_early_f32(const float *x, int64_t n, int64_t m, int64_t 
  * the float32 image of x -- which is what the reference computes, since
  * as_matrix converts every input to float32 (batch.py:30-36) -- with half
  * the input bytes and no conversion pass.  mode 0 = exact (eps_rel = 0,
- * hard_cap), 1 = early stop (max_iter); no traces.  Native path: 1 <= k < m,
- * m <= 256, m % 4 == 0, ldx % 4 == 0, x 8-byte aligned; anything else
- * returns RTK_EUNSUPPORTED (convert to float32 and use the _f32 calls). */
+ * hard_cap), 1 = early stop (max_iter); no traces.  Native path: 1 <= k < m
+ * and either m <= 256, m % 4 == 0, ldx % 4 == 0, x 8-byte aligned, or
+ * 256 < m <= 4096, m % 8 == 0, ldx % 8 == 0, x 16-byte aligned; anything
+ * else returns RTK_EUNSUPPORTED (convert to float32 and use the _f32 calls). */
 RTK_API int rtk_rowtopk_x16(const void *x, int32_t dtype, int32_t mode, int64_t n, int64_t m, int64_t ldx,
                     int32_t k, int32_t hard_cap, int32_t max_iter, float *vals, int32_t *idx,
                     int64_t ldo, uint32_t *nan_first_row, void *stream);

@@ -450,8 +450,8 @@ def batch_topk(matrix, cfg: BatchConfig) -> BatchResult:
 
 
 def topk_device(x, k: int, search: SearchConfig | None = None, nan_word=None):
-    """Row top-k of a CUDA matrix (float32; bfloat16 / float16 rows of up to
-    256 columns are read natively, others widened) enqueued on the current
+    """Row top-k of a CUDA matrix (float32; bfloat16 / float16 rows are read
+    natively where rtk_rowtopk_x16 supports the shape, others widened) enqueued on the current
     stream with no host synchronisation (capturable in a CUDA graph; the
     16-bit widening of unsupported shapes allocates): returns device
     (values, indices).  NaN rows are not raised here -- pass a 1-element

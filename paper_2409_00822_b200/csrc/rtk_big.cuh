@@ -41,9 +41,14 @@ struct BigMinCtas {
     static constexpr int value = E <= 12 ? 6 : (E <= 20 ? 5 : (E <= 32 ? (MASKED ? 3 : 4) : (wide > 0 ? wide : 1)));
 };
 
-template <int MODE, int E, bool MASKED, bool TRACES>
+// In: the input element type (float, or __nv_bfloat16 / __half for
+// rtk_rowtopk_x16: 16-bit chunks in the ring, widened when the tile is read).
+template <int MODE, int E, bool MASKED, bool TRACES, class In = float>
 __global__ void __launch_bounds__(BigThreads<E>::value, BigMinCtas<E, MASKED>::value) rowtopk_big_kernel(Args a) {
     using Row = LaneRowCut<E, MASKED>;
+    constexpr bool kF32 = std::is_same<In, float>::value;
+    constexpr unsigned kSlot = kF32 ? Row::kRowBytes : Row::kRowBytes16;
+    const In* __restrict__ x = reinterpret_cast<const In*>(a.x);
     constexpr int D = RTK_BIG_DEPTH;
     extern __shared__ __align__(16) float smem[];
     const int lane = threadIdx.x & 31;
@@ -52,23 +57,29 @@ __global__ void __launch_bounds__(BigThreads<E>::value, BigMinCtas<E, MASKED>::v
     const unsigned base = (unsigned)__cvta_generic_to_shared(smem);
     const unsigned stage_bytes = Row::stage_bytes(a.k);  // k (value, index) pairs
     const unsigned sbase = base + (unsigned)wid * stage_bytes;
-    const unsigned ring = base + wpc * stage_bytes + (unsigned)wid * D * Row::kRowBytes;
+    const unsigned ring = base + wpc * stage_bytes + (unsigned)wid * D * kSlot;
     const unsigned nw = gridDim.x * wpc;
     const unsigned long long n = (unsigned long long)a.n;
     unsigned r = blockIdx.x * wpc + (unsigned)wid;
     if (r >= n) return;
-    const unsigned ldx_b = (unsigned)a.ldx * 4u;
+    const unsigned ldx_b = (unsigned)a.ldx * (unsigned)sizeof(In);
     const bool fp = a.eps_rel == 0.0;
     if constexpr (MASKED) {  // padding chunks of the ring: NaN once (load_smem_prefilled)
 #pragma unroll
-        for (int d = 0; d < D; ++d) Row::fill_slot_nan(ring + d * Row::kRowBytes, lane);
+        for (int d = 0; d < D; ++d) Row::fill_slot_nan(ring + d * kSlot, lane, kSlot);
         __syncwarp();
     }
+    auto stage = [&](unsigned row, unsigned slot, unsigned salt) {
+        if constexpr (kF32)
+            Row::stage_async(row_ptr(x, row, ldx_b), a.m, lane, slot, salt);
+        else
+            Row::template stage_async16<In>(row_ptr(x, row, ldx_b), a.m, lane, slot, salt);
+    };
     // prologue: rows r, r + nw, ..., r + (D-1) nw
 #pragma unroll
     for (int d = 0; d < D; ++d) {
         const unsigned long long rd = (unsigned long long)r + (unsigned long long)d * nw;
-        if (rd < n) Row::stage_async(row_ptr(a.x, (unsigned)rd, ldx_b), a.m, lane, ring + d * Row::kRowBytes);
+        if (rd < n) stage((unsigned)rd, ring + d * kSlot, 0u);
         cp_async_commit();
     }
     unsigned slot = 0;
@@ -76,14 +87,17 @@ __global__ void __launch_bounds__(BigThreads<E>::value, BigMinCtas<E, MASKED>::v
     for (;;) {
         cp_async_wait<D - 1>();  // this lane's copies of this row have landed ...
         __syncwarp();            // ... and (chunks go to their owner lanes) every lane's
-        const unsigned sl = ring + slot * Row::kRowBytes;
-        row.load_smem_prefilled(sl, lane);
+        const unsigned sl = ring + slot * kSlot;
+        if constexpr (kF32)
+            row.load_smem_prefilled(sl, lane);
+        else
+            row.template load_smem16<In>(sl, lane);
         const unsigned long long rpre = (unsigned long long)r + (unsigned long long)D * nw;
         // refill after the tile has been read (the token orders the LDGSTS after the LDS)
         process_row<MODE, TRACES>(row, r, a, lane, sbase, fp, [&](unsigned tok) {
             __syncwarp();  // every lane has read its tile out of the slot before any refill lands
             const unsigned salt = tok & a.opaque_zero;
-            if (rpre < n) Row::stage_async(row_ptr(a.x, (unsigned)rpre + salt, ldx_b), a.m, lane, sl, salt);
+            if (rpre < n) stage((unsigned)rpre + salt, sl, salt);
             cp_async_commit();
         });
         if ((unsigned long long)r + nw >= n) break;

@@ -238,8 +238,10 @@ int rtk_rowtopk_x16(const void* x, int32_t dtype, int32_t mode, int64_t n, int64
     if (n > 0 && (!vals || !idx)) return fail(RTK_EINVAL, "vals/idx is NULL");
     if (mode == rtk::kExact && hard_cap < 1) return fail(RTK_EINVAL, "hard_cap must be >= 1, got %d", hard_cap);
     if (mode == rtk::kEarly && max_iter < 1) return fail(RTK_EINVAL, "max_iter must be >= 1, got %d", max_iter);
-    if (k == m || m > 256 || m % 4 != 0 || ldx % 4 != 0 || (reinterpret_cast<uintptr_t>(x) & 7) != 0 ||
-        n >= 0xffff0000LL)
+    const uintptr_t xa = reinterpret_cast<uintptr_t>(x);
+    const bool pair_ok = m <= 256 && m % 4 == 0 && ldx % 4 == 0 && (xa & 7) == 0 && n < 0xffff0000LL;
+    const bool long_ok = m > 256 && m <= 4096 && m % 8 == 0 && ldx % 8 == 0 && (xa & 15) == 0;
+    if (k == m || !(pair_ok || long_ok))
         return fail(RTK_EUNSUPPORTED, "shape outside the native 16-bit path (m=%lld, k=%d, ldx=%lld)",
                     (long long)m, k, (long long)ldx);
     cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -1,6 +1,8 @@
-// rtk_dispatch_x16.cu -- 16-bit input rows (bfloat16 / float16) on the
-// paired-row kernel: M <= 256, M % 4 == 0, 8-byte aligned rows, no traces
-// (rtk_rowtopk_x16 checks the shape; see include/rtk.h).
+// rtk_dispatch_x16.cu -- 16-bit input rows (bfloat16 / float16), no traces
+// (rtk_rowtopk_x16 checks the shape; see include/rtk.h): the paired-row
+// kernel for M <= 256 (M % 4 == 0, 8-byte aligned rows) and the long-row
+// kernel for 256 < M <= 4096 (M % 8 == 0, 16-byte aligned rows; 16-bit
+// chunks in the cp.async ring, widened when the tile is read).
 #include "rtk_dispatch.cuh"
 
 namespace {
@@ -18,9 +20,34 @@ int launch_pair16(const rtk::Args& a, cudaStream_t s) {
     return launch_rows(rtk::rowtopk_pair_kernel<MODE, E, true, false, In>, a, s, smem, kThreads, 2);
 }
 
+template <int MODE, int E, bool MASKED, class In>
+int launch_big16_kernel(const rtk::Args& a, cudaStream_t s) {
+    using namespace rtk_dispatch;
+    using Row = rtk::LaneRowCut<E, MASKED>;
+    const size_t per_warp = Row::stage_bytes(a.k) + RTK_BIG_DEPTH * Row::kRowBytes16;
+    int wpc = rtk::BigThreads<E>::value / 32;
+    while (wpc > 1 && (size_t)wpc * per_warp > kMaxSmem) --wpc;
+    return launch_rows(rtk::rowtopk_big_kernel<MODE, E, MASKED, false, In>, a, s, (size_t)wpc * per_warp, 32 * wpc);
+}
+
+template <int MODE, int E, class In>
+int launch_big16(const rtk::Args& a, cudaStream_t s) {
+    if (a.m == 32 * E) return launch_big16_kernel<MODE, E, false, In>(a, s);
+    return launch_big16_kernel<MODE, E, true, In>(a, s);
+}
+
 template <int MODE, class In>
 int dispatch16(const rtk::Args& a, cudaStream_t s) {
-    return a.m <= 128 ? launch_pair16<MODE, 4, In>(a, s) : launch_pair16<MODE, 8, In>(a, s);
+    const int m = a.m;
+    if (m <= 128) return launch_pair16<MODE, 4, In>(a, s);
+    if (m <= 256) return launch_pair16<MODE, 8, In>(a, s);
+    if (m <= 512) return launch_big16<MODE, 16, In>(a, s);
+    if (m <= 768) return launch_big16<MODE, 24, In>(a, s);
+    if (m <= 1024) return launch_big16<MODE, 32, In>(a, s);
+    if (m <= 1536) return launch_big16<MODE, 48, In>(a, s);
+    if (m <= 2048) return launch_big16<MODE, 64, In>(a, s);
+    if (m <= 3072) return launch_big16<MODE, 96, In>(a, s);
+    return launch_big16<MODE, 128, In>(a, s);
 }
 
 }  // namespace

@@ -478,6 +478,50 @@ struct LaneRow {
         }
     }
 
+    // 16-bit rows in a ring slot (long-row kernel, rtk_rowtopk_x16): lane l's
+    // E halves at l * kLaneStride16 (odd number of 16-byte chunks, as for
+    // fp32); the row is copied in 512-byte coalesced pieces, each 16-byte
+    // chunk (8 halves) sent to its owner lane.  Needs E % 8 == 0 and
+    // M % 8 == 0 (whole chunks); chunks past M are not copied (NaN-prefilled:
+    // a 0x7fff half is NaN in both formats).
+    static constexpr unsigned kChunks16 = E / 8;
+    static constexpr unsigned kLaneStride16 = 16u * (kChunks16 | 1u);
+    static constexpr unsigned kRowBytes16 = 32u * kLaneStride16;
+    template <class In>
+    __device__ __forceinline__ static void stage_async16(const In* __restrict__ p, int m, int lane, unsigned slot,
+                                                         unsigned salt = 0u) {
+        static_assert(E % 8 == 0, "16-bit staging needs whole 16-byte chunks per lane");
+        const In* src = p + 8 * lane;
+        const unsigned e0 = 8u * (unsigned)lane + (kSaltStage ? salt : 0u);
+#pragma unroll
+        for (int g = 0; g < (int)kChunks16; ++g) {
+            const unsigned e = 256u * g + e0;
+            const unsigned dst = slot + (e / E) * kLaneStride16 + 16u * ((e % E) / 8u);
+            if (!MASKED || (int)e < m) cp_async16(dst, src + 256 * g, 16u);
+        }
+    }
+    template <class In>
+    __device__ __forceinline__ void load_smem16(unsigned slot, int lane) {
+        const unsigned src = slot + (unsigned)lane * kLaneStride16;
+#pragma unroll
+        for (int g = 0; g < E / 8; ++g) {
+            const float4 q = lds128(src + 16u * g);
+            const unsigned w[4] = {__float_as_uint(q.x), __float_as_uint(q.y), __float_as_uint(q.z),
+                                   __float_as_uint(q.w)};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                if constexpr (std::is_same<In, __nv_bfloat16>::value) {
+                    v[8 * g + 2 * h] = __uint_as_float(w[h] << 16);
+                    v[8 * g + 2 * h + 1] = __uint_as_float(w[h] & 0xffff0000u);
+                } else {
+                    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[h]));
+                    v[8 * g + 2 * h] = f.x;
+                    v[8 * g + 2 * h + 1] = f.y;
+                }
+            }
+        }
+    }
+
     // Unmasked read of a slot whose padding chunks hold NaN already (see
     // fill_slot_nan): no per-element select, so the LDS results are the tile.
     __device__ __forceinline__ void load_smem_prefilled(unsigned slot, int lane) {
@@ -490,10 +534,10 @@ struct LaneRow {
     }
     // NaN into every chunk of a slot (stage_async never writes the chunks past
     // M, so they stay NaN for every row of the launch).
-    __device__ __forceinline__ static void fill_slot_nan(unsigned slot, int lane) {
+    __device__ __forceinline__ static void fill_slot_nan(unsigned slot, int lane, unsigned bytes = kRowBytes) {
         const float nan = __int_as_float(0x7fffffff);
 #pragma unroll 1
-        for (unsigned i = (unsigned)lane; i < kRowBytes / 16u; i += 32u)
+        for (unsigned i = (unsigned)lane; i < bytes / 16u; i += 32u)
             asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};" ::"r"(slot + 16u * i), "f"(nan) : "memory");
     }
 

@@ -111,7 +111,7 @@ class _MaxKDense(torch.autograd.Function):
 
 def maxk(x: torch.Tensor, k: int, search: SearchConfig | None = None, check_nan: bool = True):
     """Row top-k of a CUDA matrix (float32, or bfloat16 / float16 read
-    natively for M <= 256) as (float32 values, int32 indices); values carry
+    natively up to 4096 columns) as (float32 values, int32 indices); values carry
     the gradient (scattered back to the selected columns, in x's dtype).
     check_nan=False skips the NaN read-back (no host sync per call; the op
     can then be captured in a CUDA graph)."""

@@ -439,15 +439,16 @@ def test_launch_shape_describes_the_dispatch():
 @pytest.mark.parametrize("dtype", ["bfloat16", "float16"])
 def test_16bit_rows_native_path(oracle_lib, dtype):
     """bfloat16 / float16 CUDA matrices: M <= 256 rows are read natively by
-    rtk_rowtopk_x16 (paired-row kernel, widened in registers) and give the
-    oracle's result on the float32 image -- the reference's as_matrix
+    rtk_rowtopk_x16 (paired-row kernel, widened in registers), and so are
+    256 < M <= 4096 with M % 8 == 0 (long-row kernel, 16-bit ring); results
+    equal the oracle's on the float32 image -- the reference's as_matrix
     conversion; other shapes, traces and eps_rel > 0 widen on the device
     first.  Covers masked/unmasked/16-byte/8-byte-aligned tiles, odd N,
     strided views, NaN / inf / huge / tie-heavy rows."""
     tdt = getattr(torch, dtype)
     rng = np.random.default_rng(161)
-    for m in (4, 100, 128, 132, 200, 256, 300, 1024):
-        n = 1001
+    for m in (4, 100, 128, 132, 200, 256, 300, 264, 512, 520, 768, 1024, 1032, 2048, 3000, 4096, 5000):
+        n = 1001 if m <= 1024 else 203
         x = _mixed_rows(rng, n, m)
         xd = torch.from_numpy(x).cuda().to(tdt)
         x32 = xd.float().cpu().numpy()
@@ -455,6 +456,8 @@ def test_16bit_rows_native_path(oracle_lib, dtype):
             for mode, mi, eps in (("exact", 4, 0.0), ("early", 3, 0.0), ("exact", 4, 1e-4)):
                 want = oracle_lib.ref_batch(x32, k, mode, max_iter=mi, eps_rel=eps)
                 for t in (xd, torch.nn.functional.pad(xd, (0, 8))[:, :m]):  # contiguous, strided (ldx = m + 8)
+                    if m > 1024 and t is not xd:
+                        continue
                     for traces in (False, True):
                         res = rtk.batch_topk(t, rtk.BatchConfig(k=k, search=_search(mode, mi, eps),
                                                                 collect_traces=traces))
@@ -477,7 +480,9 @@ def test_16bit_rows_native_path(oracle_lib, dtype):
                                32, None, s) == 0
     ref = rtk.batch_topk(x.float(), rtk.BatchConfig(k=32, search=rtk.SearchConfig.early_stop(4)))
     assert torch.equal(vals, ref.values) and torch.equal(idx, ref.indices)
-    assert lib.rtk_rowtopk_x16(x.data_ptr(), code, 0, 10, 512, 512, 32, 64, 4, vals.data_ptr(), idx.data_ptr(),
-                               32, None, s) == 7  # RTK_EUNSUPPORTED: m > 256
+    assert lib.rtk_rowtopk_x16(x.data_ptr(), code, 0, 10, 516, 516, 32, 64, 4, vals.data_ptr(), idx.data_ptr(),
+                               32, None, s) == 7  # RTK_EUNSUPPORTED: m > 256 and m % 8 != 0
+    assert lib.rtk_rowtopk_x16(x.data_ptr(), code, 0, 10, 5000, 5000, 32, 64, 4, vals.data_ptr(), idx.data_ptr(),
+                               32, None, s) == 7  # RTK_EUNSUPPORTED: m > 4096
     assert lib.rtk_rowtopk_x16(x.data_ptr(), 3, 0, 10, 256, 256, 32, 64, 4, vals.data_ptr(), idx.data_ptr(),
                                32, None, s) == 1  # bad dtype

@@ -28,7 +28,11 @@ def timed(fn, steps=50, warmup=5):
 
 
 def main():
-    n, m, k = 1 << 20, 256, 32
+    for m, k in ((256, 32), (512, 64), (1024, 64), (2048, 64)):
+        run(1 << 20, m, k)
+
+
+def run(n, m, k):
     x32 = torch.randn(n, m, device="cuda")
     for mode, search in (("exact", rtk.SearchConfig.exact()), ("early4", rtk.SearchConfig.early_stop(4))):
         for name, dt in (("bf16", torch.bfloat16), ("fp16", torch.float16)):
@@ -36,11 +40,11 @@ def main():
             nat = timed(lambda: rtk.topk_device(x, k, search))
             wid = timed(lambda: rtk.topk_device(x.float(), k, search))
             gb = n * (2 * m + 8 * k) / 1e9
-            print(json.dumps({"input": name, "mode": mode, "native_ms": nat, "widen_then_f32_ms": wid,
+            print(json.dumps({"M": m, "k": k, "input": name, "mode": mode, "native_ms": nat, "widen_then_f32_ms": wid,
                               "speedup": wid / nat, "native_gbs": gb / nat * 1e3,
                               "native_frac": gb / nat * 1e3 / PEAK}))
         f = timed(lambda: rtk.topk_device(x32, k, search))
-        print(json.dumps({"input": "f32", "mode": mode, "ms": f, "frac": n * (4 * m + 8 * k) / 1e9 / f * 1e3 / PEAK}))
+        print(json.dumps({"M": m, "k": k, "input": "f32", "mode": mode, "ms": f, "frac": n * (4 * m + 8 * k) / 1e9 / f * 1e3 / PEAK}))
 
 
 if __name__ == "__main__":
