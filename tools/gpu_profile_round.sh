@@ -27,6 +27,7 @@ run_full m2048_exact exact 524288:2048:64
 run_full m2048_early early 524288:2048:64
 run_full m8192_exact exact 131072:8192:128
 timeout 900 python tools/sweep_bench.py --out $OUT/sweep.json > $OUT/sweep.log 2>&1
+timeout 600 python tools/x16_bench.py > $OUT/x16_bench.jsonl 2> $OUT/x16.err
 timeout 600 python tools/maxk_bench.py > $OUT/maxk_bench.json 2> $OUT/maxk_bench.err
 timeout 900 python tools/sweep_bench.py --shapes "1100:32,1536:64,2048:64,2500:64,3072:128,4000:64,4096:128,4500:64,6144:128,8192:128" --no-extra --no-torch --steps 30 > $OUT/sweep_long.log 2>&1
 timeout 600 python tools/file_bench.py /dev/shm > $OUT/file_bench_tmpfs.json 2> $OUT/file_bench.err
