@@ -6,6 +6,7 @@ numeric contract of the reference kernels (_kernels.py:1-10)."""
 
 from __future__ import annotations
 
+import fcntl
 import os
 import shutil
 import subprocess
@@ -50,7 +51,20 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, ex
     target = out or SO
     if out is None and not force and not needs_build():
         return SO
-    tmp = target + ".tmp"
+    # one builder at a time (every torchrun rank calls this); the others wait
+    # and then find the library current
+    with open(target + ".lock", "w") as lock:
+        fcntl.flock(lock, fcntl.LOCK_EX)
+        try:
+            if out is None and not force and not needs_build():
+                return SO
+            return _compile(target, verbose, extra)
+        finally:
+            fcntl.flock(lock, fcntl.LOCK_UN)
+
+
+def _compile(target: str, verbose: bool, extra: list[str] | None) -> str:
+    tmp = f"{target}.tmp.{os.getpid()}"
     inc = ["-I", os.path.join(ROOT, "include")]
     with tempfile.TemporaryDirectory(prefix="rtk_build_") as objdir:
         procs, objs = [], []
