@@ -32,23 +32,21 @@ def _dist():
 
 
 def sharded_batch_topk(matrix, cfg: BatchConfig, *, rank: int | None = None, world: int | None = None,
-                       local: bool = False, n_total: int | None = None, gather: bool = False, group=None,
-                       compute=None) -> tuple[BatchResult, tuple[int, int]]:
+                       local: bool = False, n_total: int | None = None, gather: bool = False,
+                       group=None) -> tuple[BatchResult, tuple[int, int]]:
     """Top-k of this rank's row block.
 
     matrix: all N rows (``local=False``; this rank slices its block) or just
     this rank's block (``local=True``, ``n_total`` = global N).  Returns
     (result, (start, stop)).  With ``gather=True`` the result holds all N rows
-    on every rank (all_gather of padded blocks, then trimmed).  ``compute``
-    defaults to :func:`batch_topk` (tests inject the CPU oracle here to
-    exercise the distribution logic without a GPU).
+    on every rank (all_gather of padded blocks, then trimmed).  The block is
+    computed by :func:`batch_topk` on this rank's current CUDA device.
     """
     dist = _dist()
     if rank is None:
         rank = dist.get_rank(group) if dist.is_initialized() else 0
     if world is None:
         world = dist.get_world_size(group) if dist.is_initialized() else 1
-    compute = compute or batch_topk
     if local:
         if n_total is None:
             raise ValueError("local=True needs n_total")
@@ -60,7 +58,7 @@ def sharded_batch_topk(matrix, cfg: BatchConfig, *, rank: int | None = None, wor
         n_total = int(matrix.shape[0])
         a, b = shard_range(n_total, rank, world)
         block = matrix[a:b]
-    res = compute(block, cfg) if b > a else None
+    res = batch_topk(block, cfg) if b > a else None
     if not gather:
         return res, (a, b)
     return _gather(res, cfg, n_total, world, group, block), (0, n_total)

@@ -3,8 +3,9 @@
 Each rank owns a contiguous row block (the reference's chunk rule,
 batch.py:87-91) and computes it with no collective; the optional gather
 reassembles all rows.  The per-rank compute is the injected CPU oracle here
-(shard.py's `compute=` hook) so the distribution plumbing is exercised
-without a GPU; on the GPU box the same code calls batch_topk."""
+(the worker replaces shard.batch_topk in its own process) so the
+distribution plumbing is exercised without a GPU; on the GPU box the same
+code calls batch_topk."""
 
 import os
 import socket
@@ -44,17 +45,20 @@ def _worker(rank, world, port, n, m, k, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2409_00822_b200 as rtk
+        from paper_2409_00822_b200 import shard
         from paper_2409_00822_b200.shard import shard_range, sharded_batch_topk
+
+        shard.batch_topk = _oracle_compute  # test-only stand-in for the GPU kernel in this CPU worker
 
         x = np.random.default_rng(123).standard_normal((n, m), dtype=np.float32)
         out = {}
         for mode, search in (("exact", rtk.SearchConfig.exact()), ("early", rtk.SearchConfig.early_stop(4))):
             cfg = rtk.BatchConfig(k=k, search=search, collect_traces=True)
-            local, (a, b) = sharded_batch_topk(x, cfg, compute=_oracle_compute)
+            local, (a, b) = sharded_batch_topk(x, cfg)
             assert (a, b) == shard_range(n, rank, world)
-            full, _ = sharded_batch_topk(x, cfg, gather=True, compute=_oracle_compute)
+            full, _ = sharded_batch_topk(x, cfg, gather=True)
             blk = x[a:b]
-            loc2, _ = sharded_batch_topk(blk, cfg, local=True, n_total=n, gather=True, compute=_oracle_compute)
+            loc2, _ = sharded_batch_topk(blk, cfg, local=True, n_total=n, gather=True)
             out[mode] = (a, b, local.indices if local is not None else None, full.values, full.indices,
                          full.trace_iterations, full.trace_reasons, loc2.indices)
         q.put((rank, out))
