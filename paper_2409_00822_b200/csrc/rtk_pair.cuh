@@ -171,7 +171,6 @@ __device__ __forceinline__ void process_pair(const Row& A, const Row& B, unsigne
         // meets cnt == k; the other continues alone.
         float midA, midB;
         int cA, cB, lA, lB, it = 0;
-        bool eqA, eqB;
 #pragma unroll 1
         do {
             ++it;
@@ -186,9 +185,10 @@ __device__ __forceinline__ void process_pair(const Row& A, const Row& B, unsigne
             mnA = ltA ? mnA : midA;
             mxB = ltB ? midB : mxB;
             mnB = ltB ? mnB : midB;
-            eqA = cA == kb;
-            eqB = cB == kb;
-        } while (!eqA && !eqB && it < steps);
+        } while (cA != kb && cB != kb && it < steps);
+        // equality taken once here: as loop-carried flags it cost two
+        // predicate instructions per pair-step (measured 2-4% in exact mode)
+        bool eqA = cA == kb, eqB = cB == kb;
         int itA = it, itB = it;
         if (!eqA && itA < steps) eqA = exact_loop_fast(A, kb, steps, mnA, mxA, midA, cA, itA, lA);
         if (!eqB && itB < steps) eqB = exact_loop_fast(B, kb, steps, mnB, mxB, midB, cB, itB, lB);
