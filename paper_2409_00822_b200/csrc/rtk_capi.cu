@@ -136,6 +136,8 @@ rtk::Args make_args(const float* x, int64_t n, int64_t m, int64_t ldx, int32_t k
     a.reasons = reinterpret_cast<signed char*>(reasons);
     a.nan_row = nan_first_row;
     a.opaque_zero = 0;
+    a.out_vec4 = vals && idx && ((reinterpret_cast<uintptr_t>(vals) | reinterpret_cast<uintptr_t>(idx)) & 15) == 0 &&
+                 ldo % 4 == 0 && k % 4 == 0 && k >= 128;  // k = 64: one half-idle iteration measured slower
     return a;
 }
 

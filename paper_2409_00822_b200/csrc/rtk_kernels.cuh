@@ -63,6 +63,9 @@ struct Args {
     // Always 0 at run time; ANDed into the next row's load offset so that the
     // load depends on the current row's lane min/max (see rowtopk_kernel).
     unsigned opaque_zero;
+    // Output rows take 16-byte stores in the paired kernel's flush: vals / idx
+    // 16-byte aligned, ldo % 4 == 0, k % 4 == 0 and k >= 128 (set by the host).
+    int out_vec4;
 };
 
 // ---------------------------------------------------------------- scalars

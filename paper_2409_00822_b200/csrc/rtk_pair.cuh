@@ -53,7 +53,7 @@ template <class Row>
 __device__ __forceinline__ void select_flush_pair(const Row& A, const Row& B, float tA, float tB, int hA, int hB,
                                                   unsigned sA, unsigned sB, int lane, int k, float* __restrict__ ovA,
                                                   int* __restrict__ oiA, float* __restrict__ ovB,
-                                                  int* __restrict__ oiB) {
+                                                  int* __restrict__ oiB, bool vec4) {
     A.stage_row(sA, lane);
     B.stage_row(sB, lane);
     const unsigned packed = (unsigned)(hA - (int)kLaneBias) | ((unsigned)(hB - (int)kLaneBias) << 16);
@@ -73,6 +73,35 @@ __device__ __forceinline__ void select_flush_pair(const Row& A, const Row& B, fl
             oiA[lane] = iA;
             ovB[lane] = xB;
             oiB[lane] = iB;
+        }
+        __syncwarp();
+        return;
+    }
+    if (vec4) {  // 4 consecutive outputs per lane: LDS.128 of indices, STG.128 stores
+#pragma unroll 1
+        for (int j = 4 * lane; j < k; j += 128) {
+            int4 iA, iB;
+            asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(iA.x), "=r"(iA.y), "=r"(iA.z), "=r"(iA.w)
+                         : "r"(sA + Row::kIdxOff + 4u * j)
+                         : "memory");
+            asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(iB.x), "=r"(iB.y), "=r"(iB.z), "=r"(iB.w)
+                         : "r"(sB + Row::kIdxOff + 4u * j)
+                         : "memory");
+            float4 xA, xB;
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xA.x) : "r"(Row::copy_addr(sA, Row::clamp_slot(iA.x))) : "memory");
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xA.y) : "r"(Row::copy_addr(sA, Row::clamp_slot(iA.y))) : "memory");
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xA.z) : "r"(Row::copy_addr(sA, Row::clamp_slot(iA.z))) : "memory");
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xA.w) : "r"(Row::copy_addr(sA, Row::clamp_slot(iA.w))) : "memory");
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xB.x) : "r"(Row::copy_addr(sB, Row::clamp_slot(iB.x))) : "memory");
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xB.y) : "r"(Row::copy_addr(sB, Row::clamp_slot(iB.y))) : "memory");
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xB.z) : "r"(Row::copy_addr(sB, Row::clamp_slot(iB.z))) : "memory");
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xB.w) : "r"(Row::copy_addr(sB, Row::clamp_slot(iB.w))) : "memory");
+            *reinterpret_cast<float4*>(ovA + j) = xA;
+            *reinterpret_cast<int4*>(oiA + j) = iA;
+            *reinterpret_cast<float4*>(ovB + j) = xB;
+            *reinterpret_cast<int4*>(oiB + j) = iB;
         }
         __syncwarp();
         return;
@@ -165,7 +194,8 @@ __device__ __forceinline__ void process_pair(const Row& A, const Row& B, unsigne
             hB = ltB ? hB : lB;
         }
         // first k indices with v >= mn (_kernels.py:205-212)
-        select_flush_pair(A, B, mnA, mnB, hA, hB, sA, sB, lane, k, ovA, oiA, ovB, oiB);
+        // (scalar flush: the vectorised one measured 2% slower in early-stop mode)
+        select_flush_pair(A, B, mnA, mnB, hA, hB, sA, sB, lane, k, ovA, oiA, ovB, oiB, false);
     } else {
         // Algorithm 1 fast steps (exact_loop_fast) on both rows until either
         // meets cnt == k; the other continues alone.
@@ -193,7 +223,7 @@ __device__ __forceinline__ void process_pair(const Row& A, const Row& B, unsigne
         if (!eqA && itA < steps) eqA = exact_loop_fast(A, kb, steps, mnA, mxA, midA, cA, itA, lA);
         if (!eqB && itB < steps) eqB = exact_loop_fast(B, kb, steps, mnB, mxB, midB, cB, itB, lB);
         if (eqA && eqB) {
-            select_flush_pair(A, B, midA, midB, lA, lB, sA, sB, lane, k, ovA, oiA, ovB, oiB);
+            select_flush_pair(A, B, midA, midB, lA, lB, sA, sB, lane, k, ovA, oiA, ovB, oiB, a.out_vec4 != 0);
         } else {
             finish_exact(A, a, lane, sA, eqA, mnA, mxA, midA, cA, itA, lA, ovA, oiA);
             finish_exact(B, a, lane, sB, eqB, mnB, mxB, midB, cB, itB, lB, ovB, oiB);

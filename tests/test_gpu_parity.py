@@ -197,7 +197,8 @@ def test_fast_paths_many_grid_steps_vs_oracle(oracle_lib):
     ring steps (and an odd tail), device-resident, no traces; sampled rows vs
     the oracle."""
     g = torch.Generator(device="cuda").manual_seed(11)
-    for n, m, k in ((300_001, 256, 32), (300_001, 128, 16), (120_001, 1024, 64), (150_001, 512, 64),
+    for n, m, k in ((300_001, 256, 32), (300_001, 128, 16), (200_001, 256, 128), (200_001, 128, 64),
+                    (120_001, 1024, 64), (150_001, 512, 64),
                     (100_003, 768, 128), (20_001, 2048, 64), (30_001, 1500, 64), (12_001, 3072, 128),
                     (10_001, 4000, 64), (9_001, 5000, 64), (9_001, 8192, 256)):
         x = torch.randn(n, m, device="cuda", generator=g)
@@ -486,3 +487,34 @@ def test_16bit_rows_native_path(oracle_lib, dtype):
                                32, None, s) == 7  # RTK_EUNSUPPORTED: m > 4096
     assert lib.rtk_rowtopk_x16(x.data_ptr(), 3, 0, 10, 256, 256, 32, 64, 4, vals.data_ptr(), idx.data_ptr(),
                                32, None, s) == 1  # bad dtype
+
+
+def test_output_row_strides_and_alignment(oracle_lib):
+    """Outputs written through the C ABI with row strides that do and do not
+    allow 16-byte stores (the paired kernel's vectorised flush for k > 32,
+    k % 4 == 0) give the same rows as a contiguous launch; padding columns
+    are untouched."""
+    rng = np.random.default_rng(9)
+    lib = rtk._native.load()
+    s = torch.cuda.current_stream().cuda_stream
+    for m, k in ((256, 64), (256, 128), (128, 64), (200, 36), (256, 33)):
+        x = rng.standard_normal((5001, m), dtype=np.float32)
+        xd = torch.from_numpy(x).cuda()
+        for mode in ("exact", "early"):
+            want = oracle_lib.ref_batch(x, k, mode, max_iter=4)
+            for ldo, off in ((k, 0), (k + 4, 0), (k + 2, 0), (k + 4, 1)):
+                vals = torch.full((5001 * ldo + 8,), 7.0, device="cuda")
+                idx = torch.full((5001 * ldo + 8,), -1, dtype=torch.int32, device="cuda")
+                vp, ip = vals[off:].data_ptr(), idx[off:].data_ptr()
+                if mode == "exact":
+                    rc = lib.rtk_rowtopk_exact_f32(xd.data_ptr(), 5001, m, m, k, 0.0, 64, vp, ip, ldo, None, None,
+                                                   None, s)
+                else:
+                    rc = lib.rtk_rowtopk_early_f32(xd.data_ptr(), 5001, m, m, k, 4, vp, ip, ldo, None, None, None, s)
+                assert rc == 0
+                v = vals[off:off + 5001 * ldo].view(5001, ldo).cpu().numpy()
+                i = idx[off:off + 5001 * ldo].view(5001, ldo).cpu().numpy()
+                ctx = (m, k, mode, ldo, off)
+                assert np.array_equal(i[:, :k], want[1]), ctx
+                assert np.array_equal(_bits(v[:, :k]), _bits(want[0])), ctx
+                assert (v[:, k:] == 7.0).all() and (i[:, k:] == -1).all(), ctx
