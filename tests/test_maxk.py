@@ -149,3 +149,25 @@ def test_topk_device_is_sync_free_and_graph_capturable():
     assert int(nan_word.item()) == 1234
     with pytest.raises(rtk.KOutOfRangeError):
         rtk.topk_device(x, m + 1)
+
+
+def test_maxk_bf16_layer_captures_in_cuda_graph():
+    """The native 16-bit path (rtk_rowtopk_x16) enqueues without host syncs
+    too: a bf16 MaxK layer captured in a CUDA graph replays equal to eager."""
+    n, m, k = 8192, 256, 16
+    static_x = torch.randn(n, m, device="cuda").to(torch.bfloat16)
+    w = torch.randn(m, 32, device="cuda").to(torch.bfloat16)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(2):
+            out = rtk.maxk_dense(static_x, k, check_nan=False) @ w
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        out = rtk.maxk_dense(static_x, k, check_nan=False) @ w
+    for trial in range(3):
+        static_x.copy_(torch.randn(n, m, device="cuda").to(torch.bfloat16))
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, rtk.maxk_dense(static_x, k) @ w), trial
