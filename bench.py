@@ -1,36 +1,50 @@
 """Benchmark of the row-wise top-k hot path on B200 (BASELINE.json configs[1]).
 
     python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
-                    [--workload c2|reddit|c5|sweep] [--mode exact|early]
+                    [--workload c2|reddit] [--mode exact|early] [--sweep]
 
 One step = one pass of the hot path (one fused kernel launch) over the whole
-synthetic batch: N = 2^20 rows x M = 256 fp32 (i.i.d. N(0,1), the reference
-generator datagen.py:49-52 run on the device), k = 32, exact mode (the
-headline) -- early stop max_iter=4 is measured in the same run and reported
-under "modes".  Inputs (1 GiB) exceed the 126 MB L2, so no flush is needed.
+batch.  The headline workload (configs[1], "c2") is N = 2^20 rows x M = 256
+fp32, k = 32, exact mode: the matrix is the reference's own generator
+(numpy default_rng(seed).standard_normal, datagen.py:49-52), built on the
+host and copied to the device before timing, and the output of the timed
+kernel is checked against the reference's digest in the
+run.  Early stop (max_iter = 4) is measured in the same run under "modes".
+The input (1 GiB) exceeds the 126 MB L2, so no flush is needed.
 
 value     rows/s of the whole job (all ranks), input resident in HBM, timed
           with CUDA events on the launching stream, max over ranks.
 e2e       the same metric through the public API batch_topk() with pinned
-          host buffers: H2D of the matrix + kernel + D2H of values/indices.
+          host input: H2D of the matrix + kernel + D2H of values/indices.
+          e2e_pageable: the reference's calling convention (a numpy array).
 roofline  HBM-bound: algorithmic bytes N*(4M + 8k) per launch / mean launch
           time vs MEASURED_PEAKS.json hbm_gbs.
-cpu_baseline  the oracle port (oracle/rtk_oracle.c, a C restatement of the
-          reference kernels) on all host cores, rank 0, N=1 only.
+cpu_baseline  the reference CPU path (its C port, oracle/rtk_oracle.c) on all
+          host cores, rank 0, N=1 only, on the first 2^18 rows.
+c5        BASELINE configs[4]: N = 2^24 x M = 512, k = 64, strong-sharded over
+          the ranks (rank r owns rows [floor(rN/G), floor((r+1)N/G)), no
+          collective), rows generated per shard on the device (blocked
+          Philox, identical whatever G); aggregate rows/s, GB/s, fraction of
+          G x peak, per-rank times and an output checksum that must not
+          depend on G.
 
-Multi-GPU (torchrun): rows are sharded with no collective; each rank runs the
-per-GPU workload on its own rows (weak scaling).
+Multi-GPU: `--gpus N` without torchrun re-launches itself under
+torch.distributed.run with N ranks (one per GPU); the headline C2 workload
+is then run by every rank on its own GPU (weak scaling).
 --impl reference: the reference CPU implementation of the path (its C port,
-since the reference is Python+numba and cannot travel to the GPU box) on the
-host cores, rank 0 only.
+the reference being Python+numba which cannot travel to the GPU box) on the
+host cores, rank 0 only, same metric/config.
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -44,9 +58,17 @@ WORKLOADS = {
     # name: (N rows per GPU, M, k)
     "c2": (1 << 20, 256, 32),
     "reddit": (232965, 256, 32),
-    "c5": (1 << 24, 512, 64),  # per-GPU share is N/G under --strong
 }
+C5 = (1 << 24, 512, 64)
 METRIC = "rows/sec and HBM GB/s of row-wise top-k (N×M fp32, k) vs torch.topk"
+# Reference digests of generate_matrix(N, M, seed=0) (SURVEY.md App. B,
+# tests/golden/digests.json): input, exact output, early-stop(4) output.
+DIGESTS = {
+    "c2": ("ebbf1d86984d665c", "f18303326eee9b0f", "e4ada2bc5c5e8969"),
+    "reddit": ("28db154966e515e9", "2ce70f5046cdbc2e", "78111f88a89b9f6b"),
+}
+SWEEP_M = (128, 256, 512, 768, 1024)
+SWEEP_K = (16, 32, 64, 128)
 
 
 def parse():
@@ -60,12 +82,24 @@ def parse():
     p.add_argument("--max-iter", type=int, default=4)
     p.add_argument("--only-mode", action="store_true", help="time only --mode (for profiling)")
     p.add_argument("--no-torch", action="store_true", help="skip the torch.topk comparison")
-    p.add_argument("--strong", action="store_true", help="shard a fixed global N across ranks")
     p.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-c5", action="store_true", help="skip the C5 strong-sharded leg")
+    p.add_argument("--c5-steps", type=int, default=20)
     p.add_argument("--seed", type=int, default=0)
-    p.add_argument("--shape", default=None, help="N:M:k (overrides --workload; for profiling sweeps)")
+    p.add_argument("--device-input", action="store_true",
+                   help="draw the input on the device (torch Philox) instead of the reference generator")
+    p.add_argument("--shape", default=None, help="N:M:k (overrides --workload; device input; for profiling)")
+    p.add_argument("--sweep", action="store_true",
+                   help="BASELINE configs[2] (M x k grid at N=2^20) + configs[3], one JSON line per cell")
     return p.parse_args()
+
+
+def h16(*arrays) -> str:
+    m = hashlib.sha256()
+    for a in arrays:
+        m.update(np.ascontiguousarray(a).tobytes())
+    return m.hexdigest()[:16]
 
 
 def peaks():
@@ -78,27 +112,36 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(workload, mode):
-    """dram bytes per launch from the committed ncu --set full capture, if any."""
+def ncu_traffic(key):
+    """DRAM bytes per launch of the hot kernel from the committed ncu --set full
+    capture (profiles/ncu_traffic.json); ncu cannot run inside a timed bench."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        return d.get(f"{workload}:{mode}")
+        v = d.get(key)
+        return (v, f"profiles/ncu_traffic.json[{key!r}] (ncu --set full capture of the same launch)") if v else (
+            None, None)
     except Exception:
-        return None
+        return None, None
 
 
 def kernel_name(m, mode):
-    """The kernel family bench's default launch dispatches to (rtk_capi.cu)."""
+    """The kernel family the default launch dispatches to (rtk_dispatch.cuh)."""
     e = ((m + 127) // 128) * 4
-    fam = "rowtopk_pair_kernel" if (m % 4 == 0 and e <= 8) else ("rowtopk_big_kernel" if m % 4 == 0 and m <= 1024
+    fam = "rowtopk_pair_kernel" if (m % 4 == 0 and e <= 8) else ("rowtopk_big_kernel" if m % 4 == 0 and m <= 4096
                                                                   else "rowtopk_kernel")
     return f"{fam}<{mode}, E={e}>"
 
 
 class ClockSampler:
     """NVML polling thread (~2 ms) for SM clocks and throttle reasons."""
+
+    _NAMES = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
 
     def __init__(self, index):
         self.index = index
@@ -118,12 +161,6 @@ class ClockSampler:
             self.ok = True
         except Exception:
             self.ok = False
-
-    _NAMES = {
-        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
-        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
-        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
-    }
 
     def _run(self):
         while not self._stop.is_set():
@@ -162,7 +199,35 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def dist_setup(args):
+# ----------------------------------------------------------------- launching
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_spawn(args) -> None:
+    """`--gpus N` without torchrun: re-launch under torch.distributed.run with
+    N ranks; under torchrun: WORLD_SIZE must equal --gpus."""
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is not None:
+        if int(world_env) != args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}; launch with matching values")
+        return
+    if args.gpus <= 1 or args.impl == "reference":
+        return
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} needs {args.gpus} CUDA devices, this node has {have}")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
+def dist_setup():
     import torch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -171,8 +236,10 @@ def dist_setup(args):
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local) if torch.cuda.is_available() else None
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        if local >= torch.cuda.device_count():
+            sys.exit(f"bench.py: rank {rank} needs cuda:{local}, this node has {torch.cuda.device_count()} devices")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
 
 
@@ -187,6 +254,28 @@ def reduce_max(x, world):
     return float(t.item())
 
 
+def all_gather_floats(x, world):
+    if world == 1:
+        return [x]
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t)
+    return [float(p.item()) for p in parts]
+
+
+def sum_u64(x, world):
+    if world == 1:
+        return x
+    import torch.distributed as dist
+
+    parts = [None] * world
+    dist.all_gather_object(parts, x)
+    return sum(parts) & 0xFFFFFFFFFFFFFFFF
+
+
 def barrier(world):
     if world > 1:
         import torch.distributed as dist
@@ -194,16 +283,9 @@ def barrier(world):
         dist.barrier()
 
 
-def make_input(n, m, seed, rank, device):
-    """N(0,1) fp32 on the device (torch Philox, per-rank seed)."""
-    import torch
-
-    g = torch.Generator(device=device).manual_seed(seed * 1000003 + rank)
-    return torch.randn((n, m), device=device, dtype=torch.float32, generator=g)
-
-
 def time_launches(fn, steps, warmup, world, stream, sampler=None):
-    """W untimed steps, then K steps between events on `stream`; returns mean ms per step (max over ranks)."""
+    """W untimed steps, then K steps between events on `stream` (barrier +
+    synchronize on both sides); mean ms per step, max over ranks."""
     import torch
 
     for _ in range(warmup):
@@ -224,8 +306,25 @@ def time_launches(fn, steps, warmup, world, stream, sampler=None):
         sampler.stop()
     barrier(world)
     ms = e0.elapsed_time(e1) / steps
-    return reduce_max(ms, world)
+    return reduce_max(ms, world), ms
 
+
+def workload_config(name, n, m, k, mode, max_iter, world, device_input):
+    """The config dict, identical in both arms for the same workload."""
+    inp = ("device torch Philox N(0,1), blocked per 2^20 rows" if device_input else
+           "numpy default_rng(seed).standard_normal float32 (reference datagen.py:49-52)")
+    big = n * m * 4 > 2 * 126e6
+    return {"workload": name, "N_per_gpu": n, "N_total": n * world, "M": m, "k": k, "mode": mode,
+            "max_iter": max_iter if mode == "early" else None, "input": inp,
+            "parallelism": f"row shards x{world} (no collective)",
+            "l2": "input > L2 (no flush needed)" if big else "input ~ L2 size: timed back to back (no flush)"}
+
+
+def reference_generator_rows(rows, m, seed):
+    return np.random.default_rng(seed).standard_normal((rows, m), dtype=np.float32)
+
+
+# ----------------------------------------------------------------- CPU arms
 
 def cpu_oracle_rate(x_np, k, mode, max_iter, threads, reps=3, budget_s=30.0):
     """Rows/s of the oracle port on the host (median of reps)."""
@@ -244,26 +343,32 @@ def cpu_oracle_rate(x_np, k, mode, max_iter, threads, reps=3, budget_s=30.0):
     return x_np.shape[0] / statistics.median(ts), reps
 
 
+def host_threads():
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+
 def run_reference(args):
-    """--impl reference: the reference CPU path (C port) on the host cores."""
+    """--impl reference: the reference CPU path (C port) on the host cores;
+    rank 0 only (other ranks exit 0 without work)."""
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return
     import oracle
 
     oracle.build()
     n, m, k = WORKLOADS[args.workload]
-    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
-    # one step = a bounded row sample of the workload, sized so the whole run stays ~2 min
+    threads = host_threads()
+    # one step = a bounded row sample of the workload (the first rows of the
+    # same generator stream), sized so the whole run stays ~2 min
     probe_rows = min(n, 1 << 16)
-    x = np.random.default_rng(args.seed).standard_normal((probe_rows, m), dtype=np.float32)
+    x = reference_generator_rows(probe_rows, m, args.seed)
     t0 = time.perf_counter()
     oracle.ref_batch(x, k, args.mode, max_iter=args.max_iter, threads=threads)
     per_row = (time.perf_counter() - t0) / probe_rows
     total_steps = args.steps + args.warmup
     rows = int(min(n, max(4096, 120.0 / max(total_steps, 1) / max(per_row, 1e-9))))
-    x = np.random.default_rng(args.seed).standard_normal((rows, m), dtype=np.float32)
+    x = reference_generator_rows(rows, m, args.seed)
     for _ in range(args.warmup):
         oracle.ref_batch(x, k, args.mode, max_iter=args.max_iter, threads=threads)
     t0 = time.perf_counter()
@@ -271,13 +376,12 @@ def run_reference(args):
         oracle.ref_batch(x, k, args.mode, max_iter=args.max_iter, threads=threads)
     dt = (time.perf_counter() - t0) / args.steps
     value = rows / dt
-    sample = f"{rows} of {n} rows x {m} fp32 N(0,1), k={k}, {args.mode} per step"
+    sample = f"first {rows} of {n} rows x {m} fp32 (same generator), k={k}, {args.mode} per step"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic N(0,1) (numpy default_rng)",
-        "config": {"workload": args.workload, "N": n, "M": m, "k": k, "mode": args.mode,
-                   "max_iter": args.max_iter if args.mode == "early" else None},
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic N(0,1) (reference generator)",
+        "config": workload_config(args.workload, n, m, k, args.mode, args.max_iter, world, args.device_input),
         "cpu_baseline": {"value": value, "unit": "rows/s", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gb_per_s": value * (4 * m + 8 * k) / 1e9,
@@ -287,32 +391,127 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------- GPU legs
+
+def c5_leg(args, rank, world, local, peak, rtk):
+    """BASELINE configs[4]: 2^24 x 512, k = 64, strong-sharded over the ranks."""
+    import torch
+
+    from paper_2409_00822_b200.shard import device_normal_rows, result_checksum, shard_range
+
+    n_tot, m, k = C5
+    a, b = shard_range(n_tot, rank, world)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    x = device_normal_rows(m, a, b, seed=args.seed, device=dev)
+    dm = rtk.batch._DeviceMatrix(x)
+    nan_word = dm._new_nan_word()
+    out = {"config": {"workload": "c5", "N_total": n_tot, "M": m, "k": k, "rows_per_rank": b - a,
+                      "input": "device torch Philox N(0,1), blocked per 2^20 rows (identical for every G)",
+                      "parallelism": f"row shards x{world}, strong scaling, no collective"}}
+    byts = (b - a) * (4 * m + 8 * k)
+    for md, s in (("exact", rtk.SearchConfig.exact()), ("early", rtk.SearchConfig.early_stop(args.max_iter))):
+        o = dm.launch_topk(k, s, False, nan_word=nan_word)
+        torch.cuda.synchronize()
+        assert int(nan_word.item()) == -1
+        cs = sum_u64(result_checksum(o[0], o[1], a), world)
+        ms_max, ms_mine = time_launches(lambda o=o, s=s: dm.launch_topk(k, s, False, outputs=o, nan_word=nan_word),
+                                        args.c5_steps, 3, world, stream)
+        per_rank = all_gather_floats(ms_mine, world)
+        agg_gbs = n_tot * (4 * m + 8 * k) / (ms_max * 1e-3) / 1e9
+        out[md] = {"ms_per_step": ms_max, "rows_per_s": n_tot / (ms_max * 1e-3), "gb_per_s": agg_gbs,
+                   "frac_of_world_peak": agg_gbs / (world * peak), "per_rank_ms": per_rank,
+                   "per_rank_gb_per_s": byts / (ms_mine * 1e-3) / 1e9, "steps": args.c5_steps,
+                   "checksum": f"{cs:016x}"}
+        del o
+    del x, dm
+    torch.cuda.empty_cache()
+    return out
+
+
+def sweep(args, rank, world, local, peak, rtk):
+    """configs[2] (M x k at N = 2^20) and configs[3] (Reddit shape), both modes,
+    device-resident Philox input; one JSON line per cell with its own clocks."""
+    import torch
+
+    from paper_2409_00822_b200.shard import device_normal_rows
+
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    cells = [(1 << 20, m_, k_) for m_ in SWEEP_M for k_ in SWEEP_K] + [(WORKLOADS["reddit"][0], 256, 32)]
+    for n, m, k in cells:
+        x = device_normal_rows(m, 0, n, seed=args.seed, device=dev)
+        dm = rtk.batch._DeviceMatrix(x)
+        nan_word = dm._new_nan_word()
+        byts = n * (4 * m + 8 * k)
+        for md, s in (("exact", rtk.SearchConfig.exact()), ("early", rtk.SearchConfig.early_stop(args.max_iter))):
+            o = dm.launch_topk(k, s, False, nan_word=nan_word)
+            with ClockSampler(local) as smp:
+                ms, _ = time_launches(lambda o=o, s=s: dm.launch_topk(k, s, False, outputs=o, nan_word=nan_word),
+                                      args.steps, args.warmup, world, stream, smp)
+                clocks = smp.summary()
+            tk = None
+            if not args.no_torch:
+                tk, _ = time_launches(lambda: torch.topk(x, k, dim=1), 5, 2, world, stream)
+            gbs = byts / (ms * 1e-3) / 1e9
+            line = {"metric": METRIC, "value": n / (ms * 1e-3), "unit": "rows/s", "n_gpus": world,
+                    "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                    "config": {"workload": "reddit" if n != 1 << 20 else "c3", "N": n, "M": m, "k": k, "mode": md,
+                               "max_iter": args.max_iter if md == "early" else None,
+                               "input": "device torch Philox N(0,1)"},
+                    "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                                 "kernel": kernel_name(m, md)},
+                    "torch_topk_ms": tk, "speedup_vs_torch_topk": (tk / ms) if tk else None, "clocks": clocks}
+            if rank == 0:
+                print(json.dumps(line), flush=True)
+            del o
+        del x, dm
+        torch.cuda.empty_cache()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
         return
+    maybe_spawn(args)
     import torch
 
     import paper_2409_00822_b200 as rtk
     from paper_2409_00822_b200 import _build, _native
 
     _build.build()
-    rank, world, local = dist_setup(args)
+    if not torch.cuda.is_available():
+        sys.exit("bench.py: no CUDA device (the product path has no CPU fallback)")
+    rank, world, local = dist_setup()
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    n_cfg, m, k = WORKLOADS[args.workload]
-    if args.shape:
-        n_cfg, m, k = (int(v) for v in args.shape.split(":"))
-        args.workload = f"custom {args.shape}"
-    n = n_cfg // world if args.strong else n_cfg
-    if args.strong:
-        from paper_2409_00822_b200.shard import shard_range
+    peak, peak_src = peaks()
+    if args.sweep:
+        sweep(args, rank, world, local, peak, rtk)
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
 
-        a, b = shard_range(n_cfg, rank, world)
-        n = b - a
+    name = args.workload
+    n, m, k = WORKLOADS[name]
+    device_input = args.device_input
+    if args.shape:
+        n, m, k = (int(v) for v in args.shape.split(":"))
+        name, device_input = f"custom {args.shape}", True
     stream = torch.cuda.current_stream(dev)
-    x = make_input(n, m, args.seed, rank, dev)
+    check = None
+    if device_input:
+        from paper_2409_00822_b200.shard import device_normal_rows
+
+        x = device_normal_rows(m, 0, n, seed=args.seed, device=dev)
+        x_np = None
+    else:
+        x_np = reference_generator_rows(n, m, args.seed)
+        if args.seed == 0 and name in DIGESTS:
+            check = DIGESTS[name]
+            assert h16(x_np) == check[0], "input differs from the reference generator's"
+        x = torch.from_numpy(x_np).to(dev)
     dm = rtk.batch._DeviceMatrix(x)
     searches = {"exact": rtk.SearchConfig.exact(), "early": rtk.SearchConfig.early_stop(args.max_iter)}
     if args.only_mode:
@@ -322,7 +521,6 @@ def main():
     torch.cuda.synchronize()
     assert int(nan_word.item()) == -1
 
-    peak, peak_src = peaks()
     bytes_per_launch = n * (4 * m + 8 * k)
     results = {}
     with ClockSampler(local) as sampler:
@@ -333,83 +531,100 @@ def main():
                 dm.launch_topk(k, s, False, outputs=o, nan_word=nan_word)
 
             smp = sampler if md == args.mode else None
-            ms = time_launches(step, args.steps, args.warmup, world, stream, smp)
+            ms, _ = time_launches(step, args.steps, args.warmup, world, stream, smp)
             results[md] = {"ms_per_step": ms, "rows_per_s": world * n / (ms * 1e-3),
                            "gb_per_s_per_gpu": bytes_per_launch / (ms * 1e-3) / 1e9,
                            "roofline_frac": bytes_per_launch / (ms * 1e-3) / 1e9 / peak}
         clocks = sampler.summary()
+    # parity of the timed launches' output (the buffers the last timed step wrote)
+    parity = {}
+    for md, o in outs.items():
+        want = None
+        if check is not None and (md == "exact" or args.max_iter == 4):
+            want = check[1] if md == "exact" else check[2]
+        got = h16(o[0].cpu().numpy(), o[1].cpu().numpy()) if want else None
+        parity[md] = {"digest": got, "reference_digest": want, "ok": (got == want) if want else None}
+        if want and got != want:
+            sys.exit(f"bench.py: {md} output digest {got} != reference {want} (parity failure)")
 
     # torch.topk on the same device-resident input (the paper's comparison point)
     tk = {}
     for sorted_ in (() if args.no_torch else (True, False)):
-        ms = time_launches(lambda: torch.topk(x, k, dim=1, sorted=sorted_), max(5, args.steps // 10),
-                           3, world, stream)
+        ms, _ = time_launches(lambda: torch.topk(x, k, dim=1, sorted=sorted_), max(5, args.steps // 10),
+                              3, world, stream)
         tk["sorted" if sorted_ else "unsorted"] = {"ms_per_step": ms, "rows_per_s": world * n / (ms * 1e-3)}
     head = results[args.mode]
     speedup_vs_torch = tk["sorted"]["ms_per_step"] / head["ms_per_step"] if tk else None
 
-    # e2e through the public API with pinned host buffers (H2D + kernel + D2H each step)
-    e2e = None
+    # e2e through the public API: pinned host input (H2D + kernel + D2H each
+    # step), and the reference's own calling convention (pageable numpy)
+    e2e = e2e_pageable = None
     if not args.no_e2e:
-        xh = x.cpu().pin_memory()
         cfg = rtk.BatchConfig(k=k, search=searches[args.mode])
         e2e_steps = max(3, min(args.steps, 10))
-        # warm-up in the timed loop's pattern (the previous result is still held
-        # during each call), so both pinned output buffer sets are cached
-        for _ in range(3):
-            res = rtk.batch_topk(xh, cfg)
-        torch.cuda.synchronize()
-        barrier(world)
-        t0 = time.perf_counter()
-        per_call = []
-        for _ in range(e2e_steps):
-            t1 = time.perf_counter()
-            res = rtk.batch_topk(xh, cfg)
-            per_call.append(round((time.perf_counter() - t1) * 1e3, 3))
-        torch.cuda.synchronize()
-        dt = reduce_max((time.perf_counter() - t0) / e2e_steps, world)
-        print(f"e2e per-call ms: {per_call}", file=sys.stderr)
+
+        def timed_calls(src):
+            for _ in range(3):  # warm-up in the timed pattern (pinned output buffers cached)
+                res = rtk.batch_topk(src, cfg)
+            torch.cuda.synchronize()
+            barrier(world)
+            t0 = time.perf_counter()
+            for _ in range(e2e_steps):
+                res = rtk.batch_topk(src, cfg)
+            torch.cuda.synchronize()
+            return reduce_max((time.perf_counter() - t0) / e2e_steps, world), res
+
+        xh = (torch.from_numpy(x_np) if x_np is not None else x.cpu()).pin_memory()
+        dt, res = timed_calls(xh)
         e2e = {"value": world * n / dt, "unit": "rows/s", "h2d_bytes_per_step": int(xh.numel() * 4),
                "d2h_bytes_per_step": int(res.values.nbytes + res.indices.nbytes + 4), "steps": e2e_steps,
-               "ms_per_step": dt * 1e3}
+               "ms_per_step": dt * 1e3, "input": "pinned torch CPU tensor"}
         del xh
+        if x_np is not None:
+            dt, res = timed_calls(x_np)
+            e2e_pageable = {"value": world * n / dt, "unit": "rows/s", "ms_per_step": dt * 1e3,
+                            "steps": e2e_steps, "input": "pageable numpy array (the reference's calling convention)"}
+        del res
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+        threads = host_threads()
         rows = min(n, 1 << 18)
-        x_np = x[:rows].cpu().numpy()
-        rate, reps = cpu_oracle_rate(x_np, k, args.mode, args.max_iter, threads)
+        x_cpu = x_np[:rows] if x_np is not None else x[:rows].cpu().numpy()
+        rate, reps = cpu_oracle_rate(np.ascontiguousarray(x_cpu), k, args.mode, args.max_iter, threads)
         cpu = {"value": rate, "unit": "rows/s", "cores": threads, "kind": "port",
                "sample": f"first {rows} rows of the workload (M={m}, k={k}, {args.mode}), median of {reps}"}
 
+    c5 = None
+    if not args.no_c5 and not args.shape:
+        del outs, dm
+        torch.cuda.empty_cache()
+        c5 = c5_leg(args, rank, world, local, peak, rtk)
+
     achieved = bytes_per_launch / (head["ms_per_step"] * 1e-3) / 1e9
+    traffic, traffic_src = ncu_traffic(f"{name}:{args.mode}")
     line = {
         "metric": METRIC, "value": head["rows_per_s"], "unit": "rows/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
-        "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic N(0,1) fp32 generated on device (torch Philox), per-rank seed",
-        "config": {"workload": args.workload, "N_per_gpu": n, "N_total": world * n, "M": m, "k": k,
-                   "mode": args.mode, "max_iter": args.max_iter if args.mode == "early" else None,
-                   "parallelism": f"row shards x{world} (no collective)",
-                   "l2": "input > L2 (no flush needed)" if n * m * 4 > 2 * 126e6 else
-                         "input ~ L2 size: timed back to back (no flush)"},
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic N(0,1) fp32: " + ("torch Philox on the device" if device_input else
+                                              "the reference generator (numpy default_rng), copied to the device"),
+        "config": workload_config(name, n, m, k, args.mode, args.max_iter, world, device_input),
         "gb_per_s": world * achieved,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": ncu_traffic(args.workload, args.mode), "peak_source": peak_src,
+                     "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                      "bytes_per_launch": bytes_per_launch, "algorithmic_bytes_per_row": 4 * m + 8 * k,
                      "kernel": kernel_name(m, args.mode)},
-        "modes": results,
+        "modes": results, "parity": parity,
         "torch_topk": tk, "speedup_vs_torch_topk_sorted": speedup_vs_torch,
-        "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": args.steps,
+        "e2e": e2e, "e2e_pageable": e2e_pageable, "cpu_baseline": cpu, "clocks": clocks,
+        "gpu_launches": args.steps, "c5": c5,
         "library": _native.library_path(),
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
-        import torch.distributed as dist
-
-        dist.destroy_process_group()
+        torch.distributed.destroy_process_group()
 
 
 if __name__ == "__main__":

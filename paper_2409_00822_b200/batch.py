@@ -242,6 +242,14 @@ def resolve_workers(workers: int | str) -> int:
     return w
 
 
+def _workers_ok(workers) -> bool:
+    try:
+        resolve_workers(workers)
+    except ValueError:
+        return False
+    return True
+
+
 @dataclass(frozen=True)
 class BatchConfig:
     """batch.py:52-57"""
@@ -416,12 +424,14 @@ def batch_topk(matrix, cfg: BatchConfig) -> BatchResult:
         xh = _host_tensor(matrix)
         k = int(cfg.k)
         m = int(xh.shape[1])
-        if k < 1 or k > m:
-            r = _DeviceMatrix(xh).first_nan_row()  # NaN is reported before the k-range error (batch.py:107-111)
+        if k < 1 or k > m or not _workers_ok(cfg.workers):
+            # NaN is reported before the k-range and workers errors (batch.py:107-112)
+            r = _DeviceMatrix(xh).first_nan_row()
             if r >= 0:
                 raise NaNInputError(f"matrix contains NaN (first offending row: {r})")
-            raise KOutOfRangeError(f"k must be in [1, {m}], got {k}")
-        resolve_workers(cfg.workers)
+            if k < 1 or k > m:
+                raise KOutOfRangeError(f"k must be in [1, {m}], got {k}")
+            resolve_workers(cfg.workers)
         vals, idx, iters, reasons, r = _host_pipeline(xh, k, cfg.search, cfg.collect_traces)
         if r >= 0:
             raise NaNInputError(f"matrix contains NaN (first offending row: {r})")
@@ -432,12 +442,13 @@ def batch_topk(matrix, cfg: BatchConfig) -> BatchResult:
 
     dm = _DeviceMatrix(matrix)
     k = int(cfg.k)
-    if k < 1 or k > dm.m:
-        r = dm.first_nan_row()  # NaN is reported before the k-range error (batch.py:107-111)
+    if k < 1 or k > dm.m or not _workers_ok(cfg.workers):
+        r = dm.first_nan_row()  # NaN is reported before the k-range and workers errors (batch.py:107-112)
         if r >= 0:
             raise NaNInputError(f"matrix contains NaN (first offending row: {r})")
-        raise KOutOfRangeError(f"k must be in [1, {dm.m}], got {k}")
-    resolve_workers(cfg.workers)
+        if k < 1 or k > dm.m:
+            raise KOutOfRangeError(f"k must be in [1, {dm.m}], got {k}")
+        resolve_workers(cfg.workers)
 
     nan_word = dm._new_nan_word()
     vals, idx, iters, reasons = dm.launch_topk(k, cfg.search, cfg.collect_traces, nan_word=nan_word)

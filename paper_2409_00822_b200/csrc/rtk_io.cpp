@@ -26,6 +26,7 @@
 #include <cstdint>
 #include <cstring>
 #include <mutex>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -44,6 +45,14 @@ struct Fd {
     int fd = -1;
     ~Fd() {
         if (fd >= 0) close(fd);
+    }
+};
+
+// A temporary output file removed on scope exit unless its path was cleared.
+struct TmpFile {
+    std::string path;
+    ~TmpFile() {
+        if (!path.empty()) unlink(path.c_str());
     }
 };
 
@@ -286,10 +295,19 @@ extern "C" int rtk_topk_file_f32(const char* matrix_path, const char* result_pat
     Buffers& B = *j.b;
     trace("buffers allocated");
 
+    // The result goes to a temporary file next to result_path, renamed over it
+    // only once every row is written and the NaN check has passed: a failing
+    // job leaves an existing result_path untouched and no partial file, as
+    // the reference (load_matrix -> batch_topk raise before save_result).
     Fd out;
+    TmpFile tmp;
     if (k_ok) {
-        out.fd = open(result_path, O_WRONLY | O_CREAT | O_TRUNC | O_CLOEXEC, 0644);
-        if (out.fd < 0) return rtk_fail(RTK_EIO, "%s: %s", result_path, strerror(errno));
+        tmp.path = std::string(result_path) + ".rtk-tmp." + std::to_string((long long)getpid());
+        out.fd = open(tmp.path.c_str(), O_WRONLY | O_CREAT | O_TRUNC | O_CLOEXEC, 0644);
+        if (out.fd < 0) {
+            tmp.path.clear();
+            return rtk_fail(RTK_EIO, "%s: %s", result_path, strerror(errno));
+        }
         unsigned char rh[kHeader];
         const uint64_t kk64 = (uint64_t)kk;
         std::memcpy(rh, kResultMagic, 4);
@@ -318,9 +336,11 @@ extern "C" int rtk_topk_file_f32(const char* matrix_path, const char* result_pat
     // buffers are reused (the D2H of chunk c+1).
     std::thread writer;
     std::atomic<int> wrc{RTK_OK};
+    std::string werr;  // the writer thread's error message (rtk_fail's buffer is thread-local)
     auto join_writer = [&] {
         if (writer.joinable()) writer.join();
-        return wrc.load();
+        const int rc = wrc.load();
+        return rc == RTK_OK ? rc : rtk_fail(rc, "%s", werr.c_str());
     };
     struct JoinAtExit {
         std::thread& t;
@@ -358,7 +378,12 @@ extern "C" int rtk_topk_file_f32(const char* matrix_path, const char* result_pat
             CU(cudaMemcpyAsync(B.pin_val[sl], B.d_val[sl], (size_t)rows * kk * 4, cudaMemcpyDeviceToHost, j.s[2]));
             CU(cudaMemcpyAsync(B.pin_idx[sl], B.d_idx[sl], (size_t)rows * kk * 4, cudaMemcpyDeviceToHost, j.s[2]));
             CU(cudaEventRecord(j.d2h[sl], j.s[2]));
-            if (c >= 1) writer = std::thread([&, c] { wrc = write_back(c - 1); });
+            if (c >= 1)
+                writer = std::thread([&, c] {
+                    const int rc = write_back(c - 1);
+                    if (rc != RTK_OK) werr = rtk_last_error();
+                    wrc = rc;
+                });
         }
     }
     if (k_ok) {
@@ -374,10 +399,16 @@ extern "C" int rtk_topk_file_f32(const char* matrix_path, const char* result_pat
         if (nan[(size_t)c] != 0xffffffffu) {
             const int64_t row = c * chunk_rows + nan[(size_t)c];
             if (dims) dims[2] = row;
-            if (k_ok) unlink(result_path);
             return rtk_fail(RTK_ENAN, "matrix contains NaN (first offending row: %lld)", (long long)row);
         }
     }
     if (!k_ok) return rtk_fail(RTK_EINVAL, "k must be in [1, %lld], got %d", (long long)m, k);
+    if (close(out.fd) != 0) {
+        out.fd = -1;
+        return rtk_fail(RTK_EIO, "%s: %s", result_path, strerror(errno));
+    }
+    out.fd = -1;
+    if (rename(tmp.path.c_str(), result_path) != 0) return rtk_fail(RTK_EIO, "%s: %s", result_path, strerror(errno));
+    tmp.path.clear();  // renamed: nothing to remove
     return RTK_OK;
 }

@@ -31,6 +31,60 @@ def _dist():
     return dist
 
 
+# Rows of a device-generated matrix come in fixed blocks of this many rows,
+# each drawn from its own Philox stream, so a shard's rows do not depend on
+# the number of shards.
+GEN_BLOCK_ROWS = 1 << 20
+
+
+def device_normal_rows(m: int, start: int, stop: int, seed: int = 0, device=None, out=None):
+    """Rows [start, stop) of a virtual N(0,1) float32 matrix with M = m
+    columns, generated on `device`: block b (rows [b*GEN_BLOCK_ROWS, ...))
+    is torch.randn from a Philox generator seeded (seed * 1000003 + b).
+    Identical rows whatever the sharding (the C5 input of SURVEY.md 8(d):
+    2^24 x 512 is generated per shard on the device, not on the host)."""
+    import torch
+
+    device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    n = stop - start
+    x = out if out is not None else torch.empty((n, m), dtype=torch.float32, device=device)
+    b0, b1 = start // GEN_BLOCK_ROWS, -(-stop // GEN_BLOCK_ROWS)
+    for b in range(b0, b1):
+        lo, hi = b * GEN_BLOCK_ROWS, (b + 1) * GEN_BLOCK_ROWS
+        a, z = max(lo, start), min(hi, stop)
+        g = torch.Generator(device=device).manual_seed(seed * 1000003 + b)
+        if a == lo and z == hi:
+            torch.randn((hi - lo, m), generator=g, device=device, dtype=torch.float32, out=x[a - start:z - start])
+        else:
+            blk = torch.randn((hi - lo, m), generator=g, device=device, dtype=torch.float32)
+            x[a - start:z - start].copy_(blk[a - lo:z - lo])
+    return x
+
+
+_C1 = 0x9E3779B97F4A7C15 - (1 << 64)  # golden-ratio multiplier as a signed int64
+_C2 = 0x632BE59BD9B4E019
+
+
+def result_checksum(values, indices, row0: int = 0) -> int:
+    """Order- and position-sensitive 64-bit checksum of a block of top-k
+    rows (values as raw fp32 bits, int32 indices) starting at global row
+    `row0`, computed on the tensors' device.  Checksums of row blocks add
+    (mod 2^64), so the checksum of a sharded run is the sum of the shards'."""
+    import torch
+
+    n, k = int(values.shape[0]), int(values.shape[1])
+    if n == 0:
+        return 0
+    dev = values.device
+    pos = (torch.arange(n, device=dev, dtype=torch.int64).unsqueeze(1) + row0) * k + torch.arange(
+        k, device=dev, dtype=torch.int64)
+    w = pos * _C1 + _C2  # wraps mod 2^64 (int64 arithmetic)
+    v = values.contiguous().view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    i = indices.to(torch.int64)
+    s = ((v * w) ^ (i * (w >> 7) + pos)).sum()
+    return int(s.item()) & 0xFFFFFFFFFFFFFFFF
+
+
 def sharded_batch_topk(matrix, cfg: BatchConfig, *, rank: int | None = None, world: int | None = None,
                        local: bool = False, n_total: int | None = None, gather: bool = False,
                        group=None) -> tuple[BatchResult, tuple[int, int]]:

@@ -291,6 +291,18 @@ def test_validation_errors():
     m[2, 5] = np.nan
     with pytest.raises(rtk.NaNInputError, match="row: 2"):
         rtk.batch_topk(m, rtk.BatchConfig(k=2))
+    # precedence dims -> NaN -> k -> workers (batch.py:106-112), host and device inputs
+    for src in (m, torch.from_numpy(m).cuda()):
+        with pytest.raises(rtk.NaNInputError, match="row: 2"):
+            rtk.batch_topk(src, rtk.BatchConfig(k=2, workers=0))
+        with pytest.raises(rtk.NaNInputError, match="row: 2"):
+            rtk.batch_topk(src, rtk.BatchConfig(k=99, workers=0))
+    m[2, 5] = 0.0
+    for src in (m, torch.from_numpy(m).cuda()):
+        with pytest.raises(rtk.KOutOfRangeError):
+            rtk.batch_topk(src, rtk.BatchConfig(k=99, workers=0))
+        with pytest.raises(ValueError, match="workers"):
+            rtk.batch_topk(src, rtk.BatchConfig(k=2, workers=0))
 
 
 def test_deterministic_and_traces_off_by_default():

@@ -92,16 +92,52 @@ def gpu():
     (1000, 256, 32, "exact", 0), (1000, 256, 32, "early", 0), (4097, 128, 16, "exact", 300),
     (777, 1024, 64, "early", 100), (333, 97, 97, "exact", 50), (5, 3, 1, "exact", 1), (2049, 512, 200, "exact", 1000),
 ])
-def test_topk_file_matches_batch_topk_bytes(gpu, tmp_path, n, m, k, search, chunk):
+def test_topk_file_matches_oracle_bytes(gpu, oracle_lib, tmp_path, n, m, k, search, chunk):
     rng = np.random.default_rng(n + m)
     x = rng.standard_normal((n, m)).astype(np.float32)
     x[:: max(1, n // 7)] = np.round(x[:: max(1, n // 7)])  # some tie-heavy rows
     src, want, got = tmp_path / "x.rtkm", tmp_path / "want.rtkr", tmp_path / "got.rtkr"
     _write_rtkm(src, x)
     cfg = rtk.BatchConfig(k=k, search=rtk.SearchConfig.exact() if search == "exact" else rtk.SearchConfig.early_stop(3))
-    rtk.save_result(rtk.batch_topk(rtk.load_matrix(src), cfg), want)
+    # the expected file is the oracle's result (the reference algorithm on
+    # the CPU) written by the reference's save_result layout
+    mode = "exact" if search == "exact" else "early"
+    v, i, _, _ = oracle_lib.ref_batch(x, k, mode, max_iter=3)
+    rtk.save_result(rtk.BatchResult(values=v, indices=i), want)
     assert rtk.topk_file(src, got, cfg, chunk_rows=chunk) == (n, m)
     assert got.read_bytes() == want.read_bytes()
+
+
+@pytest.mark.gpu
+def test_topk_file_reference_digest(gpu, tmp_path):
+    """generate_matrix(4096, 256, seed 0) as an RTKM file -> RTKR: values and
+    indices equal the reference's digest 5205a48ab4ad5986 (exact) /
+    c55e12ced7a981cb (early stop 4)."""
+    from golden_util import generate_matrix, h16
+
+    src, got = tmp_path / "x.rtkm", tmp_path / "r.rtkr"
+    rtk.save_matrix(generate_matrix(4096, 256, 0), src)
+    for search, want in ((rtk.SearchConfig.exact(), "5205a48ab4ad5986"),
+                         (rtk.SearchConfig.early_stop(4), "c55e12ced7a981cb")):
+        for chunk in (0, 1000):
+            assert rtk.topk_file(src, got, rtk.BatchConfig(k=32, search=search), chunk_rows=chunk) == (4096, 256)
+            res = rtk.load_result(got)
+            assert h16(res.values, res.indices) == want
+
+
+@pytest.mark.gpu
+def test_topk_file_failure_keeps_existing_output(gpu, tmp_path):
+    """A failing job leaves an existing result file untouched and no partial
+    or temporary file (the reference raises before save_result)."""
+    x = np.random.default_rng(2).standard_normal((500, 64)).astype(np.float32)
+    x[333, 5] = np.nan
+    src, out = tmp_path / "nan.rtkm", tmp_path / "keep.rtkr"
+    _write_rtkm(src, x)
+    out.write_bytes(b"precious")
+    with pytest.raises(rtk.NaNInputError, match="first offending row: 333\\)"):
+        rtk.topk_file(src, out, rtk.BatchConfig(k=8), chunk_rows=64)
+    assert out.read_bytes() == b"precious"
+    assert sorted(p.name for p in tmp_path.iterdir()) == ["keep.rtkr", "nan.rtkm"]
 
 
 @pytest.mark.gpu
@@ -125,7 +161,7 @@ def test_topk_file_error_precedence(gpu, tmp_path):
     _write_rtkm(nanp, x)
     with pytest.raises(rtk.NaNInputError, match="first offending row: 61\\)"):
         rtk.topk_file(nanp, out, cfg, chunk_rows=7)
-    assert not out.exists()  # the partial result is removed
+    assert not out.exists()  # no partial result
     with pytest.raises(rtk.NaNInputError):  # NaN before a bad k (batch.py:107-111)
         rtk.topk_file(nanp, out, rtk.BatchConfig(k=17), chunk_rows=7)
     ok = tmp_path / "ok.rtkm"
@@ -164,7 +200,17 @@ def test_cli_parser(tmp_path):
     assert cli.build_parser().parse_args(["gen", "--rows", "5", "--cols", "7", "--out", "o"]).seed == 0
     bad = tmp_path / "bad.rtkm"
     bad.write_bytes(b"NOPE" + bytes(20))
-    assert cli.main(["run", "--matrix", str(bad), "--k", "1", "--out", str(tmp_path / "o")]) in (1, 3)
+    assert cli.main(["run", "--matrix", str(bad), "--k", "1", "--out", str(tmp_path / "o")]) == 3
+    # argparse errors are validation errors (1), not argparse's 2 (reference cli.py:35-39)
+    assert cli.main(["run", "--matrix", "m", "--k", "x", "--out", "o"]) == 1
+    assert cli.main(["run", "--bogus"]) == 1
+    assert cli.main([]) == 1
+    # file errors come before search validation (reference cli.py:137-141)
+    assert cli.main(["run", "--matrix", str(tmp_path / "missing"), "--k", "1", "--max-iter", "0",
+                     "--mode", "early-stop", "--out", "o"]) == 3
+    tr = tmp_path / "tr.rtkm"
+    tr.write_bytes(struct.pack("<4sIQQ", b"RTKM", 1, 4, 4) + bytes(20))
+    assert cli.main(["run", "--matrix", str(tr), "--k", "1", "--hard-cap", "0", "--out", "o"]) == 3
 
 
 @pytest.mark.gpu
@@ -184,3 +230,15 @@ def test_cli_run_matches_batch_topk(tmp_path):
         assert out.read_bytes() == ref.read_bytes()
     assert cli.main(["run", "--matrix", str(tmp_path / "missing"), "--k", "1", "--out", str(out)]) == 3
     assert cli.main(["run", "--matrix", str(p), "--k", "999", "--out", str(out)]) == 1
+    # workers is validated after NaN and k, as batch_topk does (batch.py:106-112)
+    assert cli.main(["run", "--matrix", str(p), "--k", "32", "--workers", "0", "--out", str(out)]) == 1
+    x = rtk.load_matrix(p).copy()
+    x[7, 3] = np.nan
+    q = tmp_path / "nan.rtkm"
+    _write_rtkm(q, x)
+    with pytest.raises(rtk.NaNInputError):
+        cli._cmd_run(cli.build_parser().parse_args(["run", "--matrix", str(q), "--k", "999", "--workers", "0",
+                                                    "--out", str(out)]))
+    with pytest.raises(rtk.KOutOfRangeError):
+        cli._cmd_run(cli.build_parser().parse_args(["run", "--matrix", str(p), "--k", "999", "--workers", "0",
+                                                    "--out", str(out)]))
