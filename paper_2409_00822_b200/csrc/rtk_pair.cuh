@@ -46,6 +46,38 @@ __device__ __forceinline__ unsigned warp_incl_scan_nv(unsigned x) {
     return x;
 }
 
+// mid_fast of two brackets at once: one FADD2 + one FMUL2 (IEEE round to
+// nearest per half, subnormals kept: bit-identical to two mid_fast calls).
+__device__ __forceinline__ void mid_fast2(float mnA, float mxA, float mnB, float mxB, float& midA, float& midB) {
+    asm("{.reg .b64 p, q; mov.b64 p, {%2, %3}; mov.b64 q, {%4, %5}; add.rn.f32x2 p, p, q;"
+        " mul.rn.f32x2 p, p, %6; mov.b64 {%0, %1}, p;}"
+        : "=f"(midA), "=f"(midB)
+        : "f"(mnA), "f"(mnB), "f"(mxA), "f"(mxB), "l"(0x3f0000003f000000ull));
+}
+
+// Biased lane counts of both rows of a pair (A.v >= tA, B.v >= tB): the
+// compare results of element q of A and B form one f32x2 pair, so the sum
+// tree is E FADD2 (with the 2^23 bias) for both rows.
+template <class Row>
+__device__ __forceinline__ void lane_count_ge2(const Row& A, const Row& B, float tA, float tB, int& lA, int& lB) {
+    constexpr int E = Row::kSlots;
+    static_assert(E % 4 == 0, "pair count tree needs E % 4 == 0");
+    float xa[E / 2], xb[E / 2];
+#pragma unroll
+    for (int q = 0; q < E; q += 2) {
+        xa[q / 2] = set_ge(A.v[q], tA);
+        xb[q / 2] = set_ge(B.v[q], tB);
+        add2(xa[q / 2], xb[q / 2], set_ge(A.v[q + 1], tA), set_ge(B.v[q + 1], tB));
+    }
+#pragma unroll
+    for (int w = 1; w < E / 2; w *= 2)
+#pragma unroll
+        for (int q = 0; q + w < E / 2; q += 2 * w) add2(xa[q], xb[q], xa[q + w], xb[q + w]);
+    add2(xa[0], xb[0], 0x1p23f, 0x1p23f);
+    lA = __float_as_int(xa[0]);
+    lB = __float_as_int(xb[0]);
+}
+
 // Both rows selected at thresholds tA, tB with biased lane hit counts hA, hB
 // (#{v >= t} per lane): stage row copies and indices, then write the first k
 // (value, index) pairs of each row.
@@ -183,8 +215,10 @@ __device__ __forceinline__ void process_pair(const Row& A, const Row& B, unsigne
         int hA = (int)kLaneBias + Row::lane_valid(a.m, lane), hB = hA;
 #pragma unroll 1
         for (int i = 0; i < steps; ++i) {
-            const float midA = mid_fast(mnA, mxA), midB = mid_fast(mnB, mxB);
-            const int lA = A.lane_count_ge(midA), lB = B.lane_count_ge(midB);
+            float midA, midB;
+            mid_fast2(mnA, mxA, mnB, mxB, midA, midB);
+            int lA, lB;
+            lane_count_ge2(A, B, midA, midB, lA, lB);
             const bool ltA = warp_count(lA) < kb, ltB = warp_count(lB) < kb;
             mxA = ltA ? midA : mxA;
             mnA = ltA ? mnA : midA;
@@ -204,10 +238,8 @@ __device__ __forceinline__ void process_pair(const Row& A, const Row& B, unsigne
 #pragma unroll 1
         do {
             ++it;
-            midA = mid_fast(mnA, mxA);
-            midB = mid_fast(mnB, mxB);
-            lA = A.lane_count_ge(midA);
-            lB = B.lane_count_ge(midB);
+            mid_fast2(mnA, mxA, mnB, mxB, midA, midB);
+            lane_count_ge2(A, B, midA, midB, lA, lB);
             cA = warp_count(lA);
             cB = warp_count(lB);
             const bool ltA = cA < kb, ltB = cB < kb;

@@ -91,8 +91,8 @@ def test_maxk_16bit_activations(dtype, oracle_lib):
         ov, oi, _, _ = oracle_lib.ref_batch(xf, k, mode, max_iter=4)
         vals, idx = rtk.maxk(x.clone().requires_grad_(True), k, search)
         assert vals.dtype == torch.float32
-        assert np.array_equal(idx.cpu().numpy(), oi), mode
-        assert np.array_equal(vals.cpu().numpy().view(np.uint32), ov.view(np.uint32)), mode
+        assert np.array_equal(idx.detach().cpu().numpy(), oi), mode
+        assert np.array_equal(vals.detach().cpu().numpy().view(np.uint32), ov.view(np.uint32)), mode
         x1 = x.clone().requires_grad_(True)
         y1 = rtk.maxk_dense(x1, k, search)
         keep = torch.zeros(n, m, dtype=torch.bool, device="cuda").scatter_(
