@@ -97,6 +97,20 @@ RTK_API int rtk_rowtopk_x16(const void *x, int32_t dtype, int32_t mode, int64_t 
                     int32_t k, int32_t hard_cap, int32_t max_iter, float *vals, int32_t *idx,
                     int64_t ldo, uint32_t *nan_first_row, void *stream);
 
+/* Fused MaxK nonlinearity (MaxK-GNN): the row top-k of
+ * rtk_rowtopk_*_f32 / rtk_rowtopk_x16 (same vals / idx outputs) and, from the
+ * same kernel, the dense MaxK rows: dense + r*ldd holds row r of x with all
+ * but the k selected entries set to +0, in x's type (dtype 0 = float32,
+ * 1 = bfloat16, 2 = float16; selected entries are bit copies).  Replaces the
+ * select -> rtk_scatter_rows_f32 pair.  mode 0 = exact (eps_rel = 0,
+ * hard_cap), 1 = early stop (max_iter); no traces.  Native path: m = 128 or
+ * 256, 1 <= k < m, ldx a multiple of 4 with x 16-byte (float32) / 8-byte
+ * (16-bit) aligned, dense rows 16-byte aligned (8-byte for 16-bit rows of
+ * 128); anything else returns RTK_EUNSUPPORTED (use the unfused pair). */
+RTK_API int rtk_maxk_dense(const void *x, int32_t dtype, int32_t mode, int64_t n, int64_t m, int64_t ldx,
+                   int32_t k, int32_t hard_cap, int32_t max_iter, float *vals, int32_t *idx, int64_t ldo,
+                   void *dense, int64_t ldd, uint32_t *nan_first_row, void *stream);
+
 /* Exit statistics only, no selection.  Replaces
  *   _kernels.exact_trace_chunk(data, k, eps_rel, hard_cap, out_iters, out_reasons)
  *   (/root/reference/pkg/src/rowtopk/_kernels.py:217-231)

@@ -18,7 +18,7 @@ CSRC = os.path.join(PKG, "csrc")
 SO = os.path.join(PKG, "librtk.so")
 # one translation unit per mode so nvcc compiles the kernel instantiations in parallel
 SOURCES = [os.path.join(CSRC, f) for f in ("rtk_dispatch_exact.cu", "rtk_dispatch_early.cu", "rtk_dispatch_trace.cu",
-                                           "rtk_dispatch_x16.cu", "rtk_capi.cu", "rtk_maxk.cu", "rtk_io.cpp")]
+                                           "rtk_dispatch_x16.cu", "rtk_dispatch_maxk.cu", "rtk_capi.cu", "rtk_maxk.cu", "rtk_io.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("rtk_kernels.cuh", "rtk_pair.cuh", "rtk_big.cuh", "rtk_block.cuh",
                                                   "rtk_dispatch.cuh")] + [os.path.join(ROOT, "include", "rtk.h")]
 

@@ -31,6 +31,8 @@ SIGNATURES = {
     "rtk_exact_trace_f32": (ctypes.c_int, [_p, _i64, _i64, _i64, _i32, ctypes.c_double, _i32,
                                            _p, _p, _p, _p]),
     "rtk_rowtopk_x16": (ctypes.c_int, [_p, _i32, _i32, _i64, _i64, _i64, _i32, _i32, _i32, _p, _p, _i64, _p, _p]),
+    "rtk_maxk_dense": (ctypes.c_int, [_p, _i32, _i32, _i64, _i64, _i64, _i32, _i32, _i32, _p, _p, _i64, _p, _i64,
+                                      _p, _p]),
     "rtk_nan_scan_f32": (ctypes.c_int, [_p, _i64, _i64, _i64, _p, _p]),
     "rtk_row_min_max_f32": (ctypes.c_int, [_p, _i64, _i64, _i64, _p, _p, _p]),
     "rtk_count_ge_f32": (ctypes.c_int, [_p, _i64, _i64, _i64, _p, _p, _p]),

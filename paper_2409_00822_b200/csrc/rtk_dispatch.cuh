@@ -23,6 +23,7 @@ int rtk_dispatch_exact(const rtk::Args& a, cudaStream_t s);
 int rtk_dispatch_early(const rtk::Args& a, cudaStream_t s);
 int rtk_dispatch_trace(const rtk::Args& a, cudaStream_t s);
 int rtk_dispatch_x16(const rtk::Args& a, int dtype, int mode, cudaStream_t s);
+int rtk_dispatch_maxk(const rtk::Args& a, int dtype, int mode, cudaStream_t s);
 int rtk_describe_exact(const rtk::Args& a, int* shape3);
 int rtk_describe_early(const rtk::Args& a, int* shape3);
 int rtk_describe_trace(const rtk::Args& a, int* shape3);

@@ -66,6 +66,11 @@ struct Args {
     // Output rows take 16-byte stores in the paired kernel's flush: vals / idx
     // 16-byte aligned, ldo % 4 == 0, k % 4 == 0 and k >= 128 (set by the host).
     int out_vec4;
+    // Fused MaxK dense output (rtk_maxk_dense, paired kernel only): row r of
+    // x with all but the selected entries zeroed, at dense + r * ldd elements
+    // of the input type.
+    void* dense;
+    long long ldd;
 };
 
 // ---------------------------------------------------------------- scalars

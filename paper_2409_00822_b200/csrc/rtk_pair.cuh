@@ -174,6 +174,70 @@ __device__ __forceinline__ void finish_exact(const Row& row, const Args& a, int 
     select_exact(row, a, lane, sbase, true, reason, thres, mn, mx, cnt, lc, ov, oi);
 }
 
+// ------------------------------------------------------- fused MaxK rows
+//
+// rtk_maxk_dense: after a row's selection (k indices staged at
+// sbase + kIdxOff by every path: select_flush_pair, finish_exact, row_body),
+// write the dense MaxK row -- x with all but the selected entries set to
+// +0 -- straight from the register tile: the staged indices set bits of a
+// 32E-bit shared bitmap (atomic OR), then each lane stores its E contiguous
+// elements (value or zero) with vector stores in the input type (16-bit
+// rows: the tile holds their exact fp32 widening, narrowed back exactly).
+// Replaces the select -> scatter_rows pair (one launch and the N*k*8-byte
+// values/indices round trip fewer for the dense consumer).
+template <class Row>
+struct DenseBitmap {
+    static constexpr unsigned kBytes = (4u * Row::kSlots + 15u) & ~15u;  // 32E bits, 16-byte padded
+};
+
+template <class In, class Row>
+__device__ __forceinline__ void dense_row(const Row& R, unsigned sbase, const Args& a, unsigned r, int lane) {
+    constexpr int E = Row::kSlots;
+    static_assert(E == 4 || E == 8, "fused MaxK rows: E = 4 or 8 (M = 128 or 256)");
+    const unsigned bm = sbase + Row::kStageBytes;
+    if (lane < E) asm volatile("st.shared.b32 [%0], %1;" ::"r"(bm + 4u * lane), "r"(0u) : "memory");
+    __syncwarp();
+    for (int j = lane; j < a.k; j += 32) {
+        unsigned i;
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(i) : "r"(sbase + Row::kIdxOff + 4u * j) : "memory");
+        i &= 32u * E - 1u;  // NaN rows (reported, output unspecified) may stage garbage
+        asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(bm + 4u * (i >> 5)), "r"(1u << (i & 31u)) : "memory");
+    }
+    __syncwarp();
+    unsigned w;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(w) : "r"(bm + 4u * ((unsigned)(lane * E) >> 5)) : "memory");
+    const unsigned bits = w >> ((unsigned)(lane * E) & 31u);
+    float o[E];
+#pragma unroll
+    for (int q = 0; q < E; ++q) o[q] = (bits >> q) & 1u ? R.v[q] : 0.0f;
+    In* dp = row_ptr(reinterpret_cast<In*>(a.dense), r, (unsigned)(a.ldd * (long long)sizeof(In))) + lane * E;
+    if constexpr (std::is_same<In, float>::value) {
+#pragma unroll
+        for (int g = 0; g < E / 4; ++g)
+            __stcs(reinterpret_cast<float4*>(dp + 4 * g), make_float4(o[4 * g], o[4 * g + 1], o[4 * g + 2], o[4 * g + 3]));
+    } else {
+        unsigned h[E / 2];
+#pragma unroll
+        for (int q = 0; q < E / 2; ++q) {
+            In lo, hi;
+            if constexpr (std::is_same<In, __nv_bfloat16>::value) {
+                lo = __float2bfloat16_rn(o[2 * q]);
+                hi = __float2bfloat16_rn(o[2 * q + 1]);
+            } else {
+                lo = __float2half_rn(o[2 * q]);
+                hi = __float2half_rn(o[2 * q + 1]);
+            }
+            h[q] = (unsigned)*reinterpret_cast<unsigned short*>(&lo) |
+                   ((unsigned)*reinterpret_cast<unsigned short*>(&hi) << 16);
+        }
+        if constexpr (E == 8)
+            __stcs(reinterpret_cast<uint4*>(dp), make_uint4(h[0], h[1], h[2], h[3]));
+        else
+            __stcs(reinterpret_cast<uint2*>(dp), make_uint2(h[0], h[1]));
+    }
+    __syncwarp();  // the bitmap and the staging are reused by the next row
+}
+
 // mn0 < mx0 with both inside (-2^126, 2^126): non-degenerate (both modes),
 // finite (exact mode's eps_rel == 0 loop test) and overflow-free midpoints.
 // NaN compares false.
@@ -184,9 +248,9 @@ __device__ __forceinline__ bool fast_eligible(float mn0, float mx0) {
 // One pair of rows (rA = r, rB = r + nw when hasB).  `after_load(token)`
 // issues the next pair's loads once both tiles have been read.
 template <int MODE, class Row, class Hook>
-__device__ __forceinline__ void process_pair(const Row& A, const Row& B, unsigned rA, unsigned rB, bool hasB,
-                                             const Args& a, int lane, unsigned sA, unsigned sB, int steps,
-                                             const Hook& after_load) {
+__device__ __forceinline__ void process_pair_sel(const Row& A, const Row& B, unsigned rA, unsigned rB, bool hasB,
+                                                 const Args& a, int lane, unsigned sA, unsigned sB, int steps,
+                                                 const Hook& after_load) {
     float mnlA, mxlA, mnlB, mxlB;
     A.lane_min_max(a.m, lane, mnlA, mxlA);
     B.lane_min_max(a.m, lane, mnlB, mxlB);
@@ -263,6 +327,18 @@ __device__ __forceinline__ void process_pair(const Row& A, const Row& B, unsigne
     }
 }
 
+// The pair's selection, then (DENSE, rtk_maxk_dense) both fused MaxK rows.
+template <int MODE, bool DENSE, class In, class Row, class Hook>
+__device__ __forceinline__ void process_pair(const Row& A, const Row& B, unsigned rA, unsigned rB, bool hasB,
+                                             const Args& a, int lane, unsigned sA, unsigned sB, int steps,
+                                             const Hook& after_load) {
+    process_pair_sel<MODE>(A, B, rA, rB, hasB, a, lane, sA, sB, steps, after_load);
+    if constexpr (DENSE) {
+        dense_row<In>(A, sA, a, rA, lane);
+        if (hasB) dense_row<In>(B, sB, a, rB, lane);
+    }
+}
+
 // Row r of the input into a register tile: fp32 rows as they are, 16-bit
 // rows (In = __nv_bfloat16 / __half, rtk_rowtopk_x16) widened on load.
 template <class In, class Row>
@@ -276,15 +352,23 @@ __device__ __forceinline__ void load_tile(Row& R, const Args& a, unsigned r, uns
 // Persistent loop over row pairs (r, r + nw), stepping 2 nw; register
 // double buffering of the pair (the roles of the two tile pairs alternate
 // between the two unrolled halves).  In: the input element type.
-template <int MODE, int E, bool MASKED, bool WIDE, class In = float>
+// DENSE: also write the fused MaxK rows (rtk_maxk_dense; one bitmap of
+// DenseBitmap bytes after each row's staging).
+template <int E, bool DENSE>
+struct PairStage {
+    static constexpr unsigned kRowStride = LaneRow<E, false>::kStageBytes + (DENSE ? DenseBitmap<LaneRow<E, false>>::kBytes : 0u);
+    static constexpr unsigned kWarpBytes = 2u * kRowStride;
+};
+
+template <int MODE, int E, bool MASKED, bool WIDE, class In = float, bool DENSE = false>
 __global__ void __launch_bounds__(RTK_CTA_THREADS, PairMinCtas<E>::value) rowtopk_pair_kernel(Args a) {
     using Row = LaneRow<E, MASKED, WIDE>;
     extern __shared__ __align__(16) float smem[];
     const int lane = threadIdx.x & 31;
     const int wid = __shfl_sync(kFull, (int)(threadIdx.x >> 5), 0);
     const unsigned wpc = blockDim.x >> 5;
-    const unsigned sA = (unsigned)__cvta_generic_to_shared(smem) + (unsigned)wid * 2u * Row::kStageBytes;
-    const unsigned sB = sA + Row::kStageBytes;
+    const unsigned sA = (unsigned)__cvta_generic_to_shared(smem) + (unsigned)wid * PairStage<E, DENSE>::kWarpBytes;
+    const unsigned sB = sA + PairStage<E, DENSE>::kRowStride;
     const unsigned nw = gridDim.x * wpc;
     const unsigned n = (unsigned)a.n;  // the host guarantees n + 2 nw < 2^32
     unsigned r = blockIdx.x * wpc + (unsigned)wid;
@@ -298,7 +382,7 @@ __global__ void __launch_bounds__(RTK_CTA_THREADS, PairMinCtas<E>::value) rowtop
     load_tile<In>(B, a, min(r + nw, last), ldx_b, lane);
     for (;;) {
         const unsigned rn = r + 2 * nw;
-        process_pair<MODE>(A, B, r, r + nw, r + nw < n, a, lane, sA, sB, steps, [&](unsigned tok) {
+        process_pair<MODE, DENSE, In>(A, B, r, r + nw, r + nw < n, a, lane, sA, sB, steps, [&](unsigned tok) {
             tok &= oz;
             load_tile<In>(C, a, min(rn, last) + tok, ldx_b, lane);
             load_tile<In>(D, a, min(rn + nw, last) + tok, ldx_b, lane);
@@ -306,7 +390,7 @@ __global__ void __launch_bounds__(RTK_CTA_THREADS, PairMinCtas<E>::value) rowtop
         if (rn >= n) break;
         r = rn;
         const unsigned rn2 = r + 2 * nw;
-        process_pair<MODE>(C, D, r, r + nw, r + nw < n, a, lane, sA, sB, steps, [&](unsigned tok) {
+        process_pair<MODE, DENSE, In>(C, D, r, r + nw, r + nw < n, a, lane, sA, sB, steps, [&](unsigned tok) {
             tok &= oz;
             load_tile<In>(A, a, min(rn2, last) + tok, ldx_b, lane);
             load_tile<In>(B, a, min(rn2 + nw, last) + tok, ldx_b, lane);

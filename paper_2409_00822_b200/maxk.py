@@ -10,6 +10,7 @@ formats:
 
   maxk(x, k)            -> (values, indices)   differentiable in values
   maxk_dense(x, k)      -> dense N x M rows with all but the top-k zeroed
+                           (M = 128 / 256: one fused kernel, rtk_maxk_dense)
   scatter_rows(v, i, m) -> dense rows from (values, indices)   (rtk_scatter_rows_f32)
   gather_rows(d, i)     -> values at indices of dense rows     (rtk_gather_rows_f32)
   to_sparse_csr(v, i, m)-> torch.sparse_csr_tensor for torch.sparse.mm
@@ -26,7 +27,8 @@ import torch
 
 from . import _native
 from .batch import BatchConfig, batch_topk, topk_device
-from .select import SearchConfig
+from .errors import KOutOfRangeError, NaNInputError
+from .select import SearchConfig, SearchMode
 
 
 def _check_pair(values, indices):
@@ -95,9 +97,53 @@ class _MaxK(torch.autograd.Function):
         return scatter_rows(grad_values.contiguous(), indices, ctx.m).to(ctx.dtype), None, None, None
 
 
+_DTYPE_CODES = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2}
+
+
+def _fused_dense(x, k, search, check_nan):
+    """rtk_maxk_dense: selection and dense MaxK rows from one kernel (values
+    and indices as batch_topk).  None when the shape is outside its native
+    path (m = 128 / 256, aligned rows) -- the caller then selects and
+    scatters."""
+    if not (x.is_cuda and x.dim() == 2 and x.dtype in _DTYPE_CODES and x.shape[0] > 0):
+        return None
+    n, m = int(x.shape[0]), int(x.shape[1])
+    if m not in (128, 256) or x.stride(1) != 1:
+        return None
+    if search.mode is SearchMode.EXACT and search.epsilon_rel != 0.0:
+        return None
+    if not 1 <= k <= m:
+        raise KOutOfRangeError(f"k must be in [1, {m}], got {k}")
+    ldx = int(x.stride(0)) if n > 1 else m
+    vals = torch.empty((n, k), dtype=torch.float32, device=x.device)
+    idx = torch.empty((n, k), dtype=torch.int32, device=x.device)
+    dense = torch.empty((n, m), dtype=x.dtype, device=x.device)
+    word = torch.empty(1, dtype=torch.int32, device=x.device) if check_nan else None
+    mode = 0 if search.mode is SearchMode.EXACT else 1
+    with torch.cuda.device(x.device):
+        rc = _native.load().rtk_maxk_dense(x.data_ptr(), _DTYPE_CODES[x.dtype], mode, n, m, ldx, int(k),
+                                           int(search.hard_cap), int(search.max_iter), vals.data_ptr(),
+                                           idx.data_ptr(), int(k), dense.data_ptr(), m,
+                                           word.data_ptr() if word is not None else None,
+                                           torch.cuda.current_stream(x.device).cuda_stream)
+    if rc == _native.RTK_EUNSUPPORTED:
+        return None
+    _native.check(rc, "rtk_maxk_dense")
+    if word is not None:
+        r = int(word.item())
+        if r != -1:
+            raise NaNInputError(f"matrix contains NaN (first offending row: {r & 0xFFFFFFFF})")
+    return dense, vals, idx
+
+
 class _MaxKDense(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, k, search, check_nan):
+        fused = _fused_dense(x.detach(), k, search, check_nan)
+        if fused is not None:
+            dense, _, indices = fused
+            ctx.save_for_backward(indices)
+            return dense
         values, indices = _select(x.detach(), k, search, check_nan)
         ctx.save_for_backward(indices)
         return scatter_rows(values, indices, int(x.shape[1])).to(x.dtype)  # kept values are exact in x's dtype
@@ -121,8 +167,19 @@ def maxk(x: torch.Tensor, k: int, search: SearchConfig | None = None, check_nan:
 def maxk_dense(x: torch.Tensor, k: int, search: SearchConfig | None = None, check_nan: bool = True) -> torch.Tensor:
     """The MaxK nonlinearity in dense form: x with all but each row's top-k
     entries set to zero, in x's dtype (gradient flows to the kept entries
-    only)."""
+    only).  Rows of 128 or 256 take the fused kernel (rtk_maxk_dense: no
+    separate scatter pass); other shapes select and then scatter."""
     return _MaxKDense.apply(x, int(k), search or SearchConfig.exact(), bool(check_nan))
+
+
+def maxk_dense_fused(x: torch.Tensor, k: int, search: SearchConfig | None = None, check_nan: bool = True):
+    """(dense, values, indices) from the fused kernel, no autograd; raises
+    ValueError when x is outside its native path (m = 128 / 256, float32 /
+    bfloat16 / float16 CUDA rows with unit column stride)."""
+    out = _fused_dense(x, int(k), search or SearchConfig.exact(), bool(check_nan))
+    if out is None:
+        raise ValueError(f"rtk_maxk_dense: unsupported input {tuple(x.shape)} {x.dtype} (stride {tuple(x.stride())})")
+    return out
 
 
 def to_sparse_csr(values: torch.Tensor, indices: torch.Tensor, m: int) -> torch.Tensor:

@@ -178,3 +178,68 @@ def test_maxk_bf16_layer_captures_in_cuda_graph():
         g.replay()
         torch.cuda.synchronize()
         assert torch.equal(out, rtk.maxk_dense(static_x, k) @ w), trial
+
+
+def _rows(kind, n, m, dtype, g):
+    if kind == "normal":
+        return torch.randn(n, m, device="cuda", generator=g).to(dtype)
+    if kind == "ties":  # few distinct values: ties at the k-th value on most rows (fill / tie paths)
+        return torch.randint(-3, 4, (n, m), device="cuda", generator=g).to(dtype)
+    x = torch.randn(n, m, device="cuda", generator=g).to(dtype)  # signed zeros and +-inf sprinkled in
+    x[:, ::17] = -0.0
+    x[::5, 3] = float("inf")
+    x[::7, 9] = float("-inf")
+    return x
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("m", [128, 256])
+def test_maxk_dense_fused_matches_select_and_scatter(dtype, m):
+    """rtk_maxk_dense (one kernel) equals batch_topk + scatter_rows bit for bit:
+    values, indices and the dense rows in x's dtype, for exact and early-stop
+    search, normal / tie-heavy / special-value rows, odd N (unpaired last row)
+    and a strided input view."""
+    g = torch.Generator(device="cuda").manual_seed(m + _DT.index(dtype))
+    for kind in ("normal", "ties", "special"):
+        for n in (1, 2, 1001):
+            base = _rows(kind, n, m + 8, dtype, g)
+            for x in (base[:, :m].contiguous(), base[:, 4:4 + m]):
+                for k in (1, 17, 32, m - 1):
+                    for search in (rtk.SearchConfig.exact(), rtk.SearchConfig.early_stop(3)):
+                        dense, vals, idx = rtk.maxk_dense_fused(x, k, search)
+                        want = rtk.batch_topk(x, rtk.BatchConfig(k=k, search=search))
+                        assert torch.equal(idx, want.indices), (kind, n, k, search.mode)
+                        assert torch.equal(vals.view(torch.int32), want.values.view(torch.int32)), (kind, n, k)
+                        sc = rtk.scatter_rows(want.values, want.indices, m).to(dtype)
+                        assert dense.dtype == dtype
+                        assert torch.equal(dense.view(torch.int16 if dtype != torch.float32 else torch.int32),
+                                           sc.view(torch.int16 if dtype != torch.float32 else torch.int32)), (kind, n, k)
+
+
+_DT = [torch.float32, torch.bfloat16, torch.float16]
+
+
+def test_maxk_dense_fused_errors_and_fallback():
+    x = torch.randn(64, 256, device="cuda")
+    x[9, 100] = float("nan")
+    x[40, 3] = float("nan")
+    with pytest.raises(rtk.NaNInputError, match="first offending row: 9"):
+        rtk.maxk_dense_fused(x, 8)
+    with pytest.raises(rtk.KOutOfRangeError):
+        rtk.maxk_dense_fused(torch.randn(4, 128, device="cuda"), 0)
+    with pytest.raises(ValueError, match="unsupported"):
+        rtk.maxk_dense_fused(torch.randn(4, 200, device="cuda"), 8)  # m outside {128, 256}
+    y = torch.randn(300, 200, device="cuda")  # maxk_dense falls back to select + scatter
+    assert torch.equal(rtk.maxk_dense(y, 9), _torch_maxk_dense(y, 9))
+
+
+def test_maxk_dense_uses_fused_kernel_and_grads():
+    """maxk_dense on 256-wide rows goes through the fused kernel (same
+    output as the formulation, gradients to the kept entries)."""
+    n, m, k = 4096, 256, 32
+    x = torch.randn(n, m, device="cuda", requires_grad=True)
+    y = rtk.maxk_dense(x, k)
+    assert torch.equal(y, _torch_maxk_dense(x.detach(), k))
+    g = torch.randn(n, m, device="cuda")
+    (y * g).sum().backward()
+    assert torch.equal(x.grad, torch.where(y != 0, g, torch.zeros((), device="cuda")))

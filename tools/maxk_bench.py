@@ -40,9 +40,21 @@ def main():
         ga = t_ms(lambda: rtk.gather_rows(x, i))
         tg = t_ms(lambda: torch.gather(x, 1, il))
         sb, gb = n * (4 * m + 8 * k), n * 12 * k  # algorithmic bytes: dense write + pairs read / idx+vals
-        out["cases"].append({"N": n, "M": m, "k": k, "scatter_ms": sc, "scatter_frac": sb / (sc * 1e-3) / 1e9 / peak,
-                             "torch_zero_scatter_ms": ts, "gather_ms": ga, "torch_gather_ms": tg,
-                             "gather_algorithmic_GBps": gb / (ga * 1e-3) / 1e9})
+        case = {"N": n, "M": m, "k": k, "scatter_ms": sc, "scatter_frac": sb / (sc * 1e-3) / 1e9 / peak,
+                "torch_zero_scatter_ms": ts, "gather_ms": ga, "torch_gather_ms": tg,
+                "gather_algorithmic_GBps": gb / (ga * 1e-3) / 1e9}
+        if m in (128, 256):
+            # MaxK forward: fused kernel vs select (topk_device) + scatter, and
+            # the plain torch formulation (topk + zeros + scatter)
+            for md, s in (("exact", rtk.SearchConfig.exact()), ("early", rtk.SearchConfig.early_stop(4))):
+                fu = t_ms(lambda: rtk.maxk_dense_fused(x, k, s, check_nan=False))
+                un = t_ms(lambda: rtk.scatter_rows(*rtk.topk_device(x, k, s), m))
+                fb = n * (8 * m + 8 * k)  # read row, write dense row + values + indices
+                case[f"fused_{md}_ms"] = fu
+                case[f"fused_{md}_frac"] = fb / (fu * 1e-3) / 1e9 / peak
+                case[f"select_scatter_{md}_ms"] = un
+            case["torch_topk_scatter_ms"] = t_ms(lambda: torch.zeros_like(x).scatter_(1, *reversed(torch.topk(x, k, dim=1))), 10)
+        out["cases"].append(case)
         del x, dense
         torch.cuda.empty_cache()
     print(json.dumps(out))

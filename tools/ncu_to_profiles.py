@@ -25,6 +25,10 @@ CAPTURES = {  # capture -> (bench workload key, rows)
     "m2048_exact": ("custom 524288:2048:64:exact", 1 << 19),
     "m2048_early": ("custom 524288:2048:64:early", 1 << 19),
     "m8192_exact": ("custom 131072:8192:128:exact", 1 << 17),
+    "m128_exact": ("custom 1048576:128:32:exact", 1 << 20),
+    "m128_early": ("custom 1048576:128:32:early", 1 << 20),
+    "m768_exact": ("custom 1048576:768:64:exact", 1 << 20),
+    "m768_early": ("custom 1048576:768:64:early", 1 << 20),
 }
 RAW_KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
             "sm__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__issue_active.avg.pct_of_peak_sustained_active",
