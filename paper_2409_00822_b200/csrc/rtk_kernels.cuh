@@ -684,16 +684,23 @@ struct LaneRow {
     }
 };
 
-// Lane-contiguous tile with cut-off selection staging: only the first k
-// output positions are staged, as (value, index) pairs (8k bytes per warp,
-// flushed by flush_row), so long rows need little shared memory.  Used by
-// the big-row kernel (rtk_big.cuh).
+// Lane-contiguous tile with cut-off selection staging: only lanes whose
+// first hit falls among the first k output positions stage their hits, as
+// (value, index) pairs; the lane straddling position k stages all of its
+// hits into E pairs of slack, so no per-element cut-off test is needed
+// (8(k + E) bytes per warp, the first k flushed by flush_row).  Long rows
+// need little shared memory.  Used by the big-row kernel (rtk_big.cuh).
+#ifndef RTK_CUT_SLACK
+#define RTK_CUT_SLACK 1
+#endif
 template <int E, bool MASKED>
 struct LaneRowCut : LaneRow<E, MASKED, false> {
     using Base = LaneRow<E, MASKED, false>;
     using Base::v;
-    static constexpr int kPad = 0;  // staging holds exactly k pairs (flush_row)
-    __host__ __device__ static constexpr unsigned stage_bytes(int k) { return (8u * (unsigned)k + 15u) & ~15u; }
+    static constexpr int kPad = 0;  // flush_row writes the first k staged pairs
+    __host__ __device__ static constexpr unsigned stage_bytes(int k) {
+        return (8u * (unsigned)(k + (RTK_CUT_SLACK ? E : 0)) + 15u) & ~15u;
+    }
 
     // Staging addresses are computed a group of G slots ahead of the stores
     // and all kept live until the group's stores have issued (folded into the
@@ -706,6 +713,7 @@ struct LaneRowCut : LaneRow<E, MASKED, false> {
         const unsigned excl = warp_incl_scan(cl) - cl;
         unsigned addr = sbase + 8u * excl;
         const unsigned aend = sbase + 8u * (unsigned)k;
+        const bool lane_on = excl < (unsigned)k;  // this lane's hits start before position k
         const int i0 = lane * E;
         unsigned sink = 0;
 #pragma unroll
@@ -715,7 +723,7 @@ struct LaneRowCut : LaneRow<E, MASKED, false> {
 #pragma unroll
             for (int q = 0; q < G; ++q) {
                 const bool hit = v[g + q] >= t;
-                p[q] = hit && addr < aend;
+                p[q] = hit && (RTK_CUT_SLACK ? lane_on : addr < aend);
                 ad[q] = addr;
                 addr += hit ? 8u : 0u;
             }
