@@ -99,17 +99,23 @@ RTK_API int rtk_rowtopk_x16(const void *x, int32_t dtype, int32_t mode, int64_t 
 
 /* Fused MaxK nonlinearity (MaxK-GNN): the row top-k of
  * rtk_rowtopk_*_f32 / rtk_rowtopk_x16 (same vals / idx outputs) and, from the
- * same kernel, the dense MaxK rows: dense + r*ldd holds row r of x with all
- * but the k selected entries set to +0, in x's type (dtype 0 = float32,
- * 1 = bfloat16, 2 = float16; selected entries are bit copies).  Replaces the
- * select -> rtk_scatter_rows_f32 pair.  mode 0 = exact (eps_rel = 0,
+ * same kernel,
+ *   - dense (nullable): the dense MaxK rows, dense + r*ldd holding row r of x
+ *     with all but the k selected entries set to +0, in x's type (dtype 0 =
+ *     float32, 1 = bfloat16, 2 = float16; selected entries are bit copies);
+ *     replaces the select -> rtk_scatter_rows_f32 pair;
+ *   - idx8 (nullable): the indices again as uint8 (m <= 256), row r at
+ *     idx8 + r*ld8 (ld8 >= k): the compact index layout of the MaxK sparse
+ *     rows consumed by rtk_maxk_spmm_f32.
+ * At least one of dense / idx8 is non-NULL.  mode 0 = exact (eps_rel = 0,
  * hard_cap), 1 = early stop (max_iter); no traces.  Native path: m = 128 or
  * 256, 1 <= k < m, ldx a multiple of 4 with x 16-byte (float32) / 8-byte
  * (16-bit) aligned, dense rows 16-byte aligned (8-byte for 16-bit rows of
  * 128); anything else returns RTK_EUNSUPPORTED (use the unfused pair). */
 RTK_API int rtk_maxk_dense(const void *x, int32_t dtype, int32_t mode, int64_t n, int64_t m, int64_t ldx,
                    int32_t k, int32_t hard_cap, int32_t max_iter, float *vals, int32_t *idx, int64_t ldo,
-                   void *dense, int64_t ldd, uint32_t *nan_first_row, void *stream);
+                   void *dense, int64_t ldd, uint8_t *idx8, int64_t ld8, uint32_t *nan_first_row,
+                   void *stream);
 
 /* Exit statistics only, no selection.  Replaces
  *   _kernels.exact_trace_chunk(data, k, eps_rel, hard_cap, out_iters, out_reasons)
@@ -146,6 +152,26 @@ RTK_API int rtk_scatter_rows_f32(const float *vals, const int32_t *idx, int64_t 
                          int64_t m, float *out, int64_t ldo, void *stream);
 RTK_API int rtk_gather_rows_f32(const float *dense, int64_t ldd, const int32_t *idx, int64_t ldv, int64_t n,
                         int32_t k, int64_t m, float *vals, void *stream);
+
+/* MaxK-GNN aggregation over the fixed-k rows (the consumer of the row top-k
+ * output): with the graph as CSR (row_ptr[n+1] int64, col int32,
+ * aval f32 edge weights, NULL = all 1) and H the fixed-k matrix (row j: vals
+ * at columns idx, k per row, row stride ldv; idx int32 or idx8 uint8 for
+ * m <= 256 -- exactly one non-NULL),
+ *   rtk_maxk_spmm_f32:          out[i, :] = sum_{e=(i,j)} aval[e] * H[j, :]
+ *                               (out n x m, row stride ldo; m <= 1024);
+ *   rtk_maxk_spmm_backward_f32: grad_vals[j, t] = sum_{e=(i,j)} aval[e] *
+ *                               grad_out[i, idx[j, t]], over the TRANSPOSED
+ *                               graph's CSR (row j lists the i with e=(i,j)).
+ * Sums run in edge order with fp32 rounding per product and per addition
+ * (deterministic).  Columns outside [0, m) are skipped. */
+RTK_API int rtk_maxk_spmm_f32(const int64_t *row_ptr, const int32_t *col, const float *aval, int64_t n,
+                      const float *vals, const int32_t *idx, const uint8_t *idx8, int64_t ldv, int32_t k,
+                      int64_t m, float *out, int64_t ldo, void *stream);
+RTK_API int rtk_maxk_spmm_backward_f32(const int64_t *row_ptr_t, const int32_t *col_t, const float *aval_t,
+                               int64_t n, const float *grad_out, int64_t ldg, const int32_t *idx,
+                               const uint8_t *idx8, int64_t ldv, int32_t k, int64_t m, float *grad_vals,
+                               void *stream);
 
 /* File-level job: RTKM matrix file -> row top-k on the current CUDA device
  * -> RTKR result file, streamed in chunks of `chunk_rows` rows (0 = ~64 MB):

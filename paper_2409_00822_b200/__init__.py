@@ -45,7 +45,9 @@ from .experiments import (  # noqa: F401
     trial_row,
 )
 from .io import load_matrix, load_result, save_matrix, save_result, topk_file  # noqa: F401
-from .maxk import gather_rows, maxk, maxk_dense, maxk_dense_fused, scatter_rows, to_sparse_csr  # noqa: F401
+from .maxk import (  # noqa: F401
+    csr_transpose, gather_rows, maxk, maxk_aggregate, maxk_dense, maxk_dense_fused, maxk_sparse_u8, maxk_spmm,
+    scatter_rows, to_sparse_csr)
 from .select import (  # noqa: F401
     DEFAULT_HARD_CAP,
     DEFAULT_MAX_ITER,
@@ -68,7 +70,7 @@ __all__ = [
     "REGISTER_COLS_LIMIT", "RowTopKError", "SOFT_COLS_LIMIT", "SearchConfig", "SearchMode", "SearchTrace",
     "TopKResult", "as_matrix", "as_row", "batch_topk", "chunk_ranges", "count_ge", "early_stop_topk",
     "exact_topk", "exact_trace", "min_max", "oracle_topk", "resolve_workers", "load_matrix", "load_result",
-    "save_matrix", "save_result", "topk_file", "topk_device", "maxk", "maxk_dense", "maxk_dense_fused", "scatter_rows", "gather_rows", "to_sparse_csr",
+    "save_matrix", "save_result", "topk_file", "topk_device", "maxk", "maxk_dense", "maxk_dense_fused", "maxk_sparse_u8", "maxk_spmm", "maxk_aggregate", "csr_transpose", "scatter_rows", "gather_rows", "to_sparse_csr",
     "DataGenSpec", "EarlyStopStats", "early_stop_experiment", "early_stop_grid", "early_stop_grid_matrix",
     "exit_iteration_grid", "exit_iteration_grid_matrix", "generate_matrix", "trial_block", "trial_row",
 ]

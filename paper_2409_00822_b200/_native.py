@@ -32,7 +32,7 @@ SIGNATURES = {
                                            _p, _p, _p, _p]),
     "rtk_rowtopk_x16": (ctypes.c_int, [_p, _i32, _i32, _i64, _i64, _i64, _i32, _i32, _i32, _p, _p, _i64, _p, _p]),
     "rtk_maxk_dense": (ctypes.c_int, [_p, _i32, _i32, _i64, _i64, _i64, _i32, _i32, _i32, _p, _p, _i64, _p, _i64,
-                                      _p, _p]),
+                                      _p, _i64, _p, _p]),
     "rtk_nan_scan_f32": (ctypes.c_int, [_p, _i64, _i64, _i64, _p, _p]),
     "rtk_row_min_max_f32": (ctypes.c_int, [_p, _i64, _i64, _i64, _p, _p, _p]),
     "rtk_count_ge_f32": (ctypes.c_int, [_p, _i64, _i64, _i64, _p, _p, _p]),
@@ -40,6 +40,8 @@ SIGNATURES = {
                                          _i64, _p]),
     "rtk_scatter_rows_f32": (ctypes.c_int, [_p, _p, _i64, _i64, _i32, _i64, _p, _i64, _p]),
     "rtk_gather_rows_f32": (ctypes.c_int, [_p, _i64, _p, _i64, _i64, _i32, _i64, _p, _p]),
+    "rtk_maxk_spmm_f32": (ctypes.c_int, [_p, _p, _p, _i64, _p, _p, _p, _i64, _i32, _i64, _p, _i64, _p]),
+    "rtk_maxk_spmm_backward_f32": (ctypes.c_int, [_p, _p, _p, _i64, _p, _i64, _p, _p, _i64, _i32, _i64, _p, _p]),
     "rtk_last_error": (ctypes.c_char_p, []),
     "rtk_version": (ctypes.c_int, []),
     "rtk_launch_shape": (ctypes.c_int, [_i64, _i32, _i32, _p, _p, _p]),

@@ -138,6 +138,8 @@ rtk::Args make_args(const float* x, int64_t n, int64_t m, int64_t ldx, int32_t k
     a.opaque_zero = 0;
     a.dense = nullptr;
     a.ldd = 0;
+    a.idx8 = nullptr;
+    a.ld8 = 0;
     a.out_vec4 = vals && idx && ((reinterpret_cast<uintptr_t>(vals) | reinterpret_cast<uintptr_t>(idx)) & 15) == 0 &&
                  ldo % 4 == 0 && k % 4 == 0 && k >= 128;  // k = 64: one half-idle iteration measured slower
     return a;
@@ -260,7 +262,7 @@ int rtk_rowtopk_x16(const void* x, int32_t dtype, int32_t mode, int64_t n, int64
 
 int rtk_maxk_dense(const void* x, int32_t dtype, int32_t mode, int64_t n, int64_t m, int64_t ldx, int32_t k,
                    int32_t hard_cap, int32_t max_iter, float* vals, int32_t* idx, int64_t ldo, void* dense,
-                   int64_t ldd, uint32_t* nan_first_row, void* stream) {
+                   int64_t ldd, uint8_t* idx8, int64_t ld8, uint32_t* nan_first_row, void* stream) {
     if (dtype < 0 || dtype > 2) return fail(RTK_EINVAL, "dtype must be 0 (float32), 1 (bfloat16) or 2 (float16), got %d", dtype);
     if (mode != rtk::kExact && mode != rtk::kEarly) return fail(RTK_EINVAL, "mode must be 0 or 1, got %d", mode);
     int rc = check_common(static_cast<const float*>(x), n, m, ldx);
@@ -268,8 +270,11 @@ int rtk_maxk_dense(const void* x, int32_t dtype, int32_t mode, int64_t n, int64_
     if (k < 1 || k > m) return fail(RTK_EINVAL, "k must be in [1, %lld], got %d", (long long)m, k);
     if (ldo < k) return fail(RTK_EINVAL, "ldo (%lld) < k (%d)", (long long)ldo, k);
     if (ldo >= (1LL << 30)) return fail(RTK_EINVAL, "ldo must be < 2^30, got %lld", (long long)ldo);
-    if (ldd < m || ldd >= (1LL << 30)) return fail(RTK_EINVAL, "ldd must be in [m, 2^30), got %lld", (long long)ldd);
-    if (n > 0 && (!vals || !idx || !dense)) return fail(RTK_EINVAL, "vals/idx/dense is NULL");
+    if (dense && (ldd < m || ldd >= (1LL << 30)))
+        return fail(RTK_EINVAL, "ldd must be in [m, 2^30), got %lld", (long long)ldd);
+    if (idx8 && (ld8 < k || ld8 >= (1LL << 30))) return fail(RTK_EINVAL, "ld8 must be in [k, 2^30), got %lld", (long long)ld8);
+    if (n > 0 && (!vals || !idx)) return fail(RTK_EINVAL, "vals/idx is NULL");
+    if (!dense && !idx8) return fail(RTK_EINVAL, "dense and idx8 are both NULL (use rtk_rowtopk_*)");
     if (mode == rtk::kExact && hard_cap < 1) return fail(RTK_EINVAL, "hard_cap must be >= 1, got %d", hard_cap);
     if (mode == rtk::kEarly && max_iter < 1) return fail(RTK_EINVAL, "max_iter must be >= 1, got %d", max_iter);
     // native path: the paired-row kernel on unmasked tiles, vector loads and
@@ -279,8 +284,9 @@ int rtk_maxk_dense(const void* x, int32_t dtype, int32_t mode, int64_t n, int64_
     const uintptr_t xa = dtype == 0 ? 16 : 8;
     const uintptr_t da = (dtype != 0 && m == 128) ? 8 : 16;
     const int64_t dq = (int64_t)da / (dtype == 0 ? 4 : 2);
-    const bool ok = (m == 128 || m == 256) && k < m && n < 0xffff0000LL && ldx % 4 == 0 && ldd % dq == 0 &&
-                    (reinterpret_cast<uintptr_t>(x) % xa) == 0 && (reinterpret_cast<uintptr_t>(dense) % da) == 0;
+    const bool ok = (m == 128 || m == 256) && k < m && n < 0xffff0000LL && ldx % 4 == 0 &&
+                    (reinterpret_cast<uintptr_t>(x) % xa) == 0 &&
+                    (!dense || (ldd % dq == 0 && (reinterpret_cast<uintptr_t>(dense) % da) == 0));
     if (!ok)
         return fail(RTK_EUNSUPPORTED, "shape outside the fused MaxK path (m=%lld, k=%d, ldx=%lld, ldd=%lld)",
                     (long long)m, k, (long long)ldx, (long long)ldd);
@@ -293,6 +299,8 @@ int rtk_maxk_dense(const void* x, int32_t dtype, int32_t mode, int64_t n, int64_
     a.max_iter = max_iter;
     a.dense = dense;
     a.ldd = ldd;
+    a.idx8 = idx8;
+    a.ld8 = ld8;
     return rtk_dispatch_maxk(a, dtype, mode, s);
 }
 

@@ -71,6 +71,9 @@ struct Args {
     // of the input type.
     void* dense;
     long long ldd;
+    // ... and / or the selected indices as uint8 (M <= 256), row r at idx8 + r * ld8.
+    unsigned char* idx8;
+    long long ld8;
 };
 
 // ---------------------------------------------------------------- scalars

@@ -13,6 +13,14 @@
 // memory in 1024-column tiles so each output line is written once with
 // 128-bit stores.  Indices outside [0, m) are ignored (scatter) / read as 0
 // (gather).
+// And the aggregation that consumes the fixed-k rows (MaxK-GNN's SpMM with
+// the top-k-processed right-hand matrix):
+//   rtk_maxk_spmm_f32: out[i, :] = sum over edges e = (i, j) of a_e * H_j,
+//     H_j the fixed-k row j (vals[j, :] at columns idx[j, :], int32 or uint8);
+//   rtk_maxk_spmm_backward_f32: grad_vals[j, t] = sum over edges (i, j) of
+//     a_e * grad_out[i, idx[j, t]] (over the transposed graph's CSR).
+// Per edge only the k (value, column) pairs of row j are read (k*(4+4) or
+// k*(4+1) bytes instead of the dense row's 4*m), which is MaxK-GNN's point.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -74,6 +82,130 @@ __global__ void __launch_bounds__(kWarps * 32) gather_rows_kernel(const float* _
     }
 }
 
+
+constexpr int kSpmmWarps = 8;  // warps per CTA of the aggregation kernels
+constexpr int kSpmmMaxM = 1024;
+
+// Index of entry t of fixed-k row j: int32 or uint8 storage.
+__device__ __forceinline__ int fixed_col(const int32_t* __restrict__ idx, const uint8_t* __restrict__ idx8,
+                                         int64_t off) {
+    return idx8 ? (int)idx8[off] : (int)idx[off];
+}
+
+// One warp per output row i; the m-float accumulator lives in the warp's
+// shared-memory row.  Edges are taken 32 at a time (lane l loads edge
+// e0 + l's column and weight, broadcast by SHFL), and for each edge every
+// lane t < k adds a_e * vals[j, t] at column idx[j, t] with a shared-memory
+// RED.ADD -- the k columns of one row are distinct, so no two lanes of one
+// instruction collide, and the warp's REDs reach the shared memory in issue
+// order: the sum is taken in edge order, deterministically.  Four edges'
+// loads are issued before their REDs to overlap the L2 latency.
+__global__ void __launch_bounds__(kSpmmWarps * 32) maxk_spmm_kernel(
+    const int64_t* __restrict__ rp, const int32_t* __restrict__ col, const float* __restrict__ aval, int64_t n,
+    const float* __restrict__ vals, const int32_t* __restrict__ idx, const uint8_t* __restrict__ idx8, int64_t ldv,
+    int32_t k, int32_t m, float* __restrict__ out, int64_t ldo) {
+    __shared__ __align__(16) float acc_s[kSpmmWarps][kSpmmMaxM];
+    const int lane = threadIdx.x & 31;
+    const int w = threadIdx.x >> 5;
+    float* acc = acc_s[w];
+    const unsigned acc_base = (unsigned)__cvta_generic_to_shared(acc);
+    const int64_t nw = (int64_t)gridDim.x * kSpmmWarps;
+    for (int64_t i = (int64_t)blockIdx.x * kSpmmWarps + w; i < n; i += nw) {
+        for (int c = lane; c < m; c += 32) acc[c] = 0.0f;
+        __syncwarp();
+        const int64_t e_beg = rp[i], e_end = rp[i + 1];
+        for (int64_t e0 = e_beg; e0 < e_end; e0 += 32) {
+            const int ne = (int)((e_end - e0) < 32 ? (e_end - e0) : 32);
+            int jl = 0;
+            float al = 0.0f;
+            if (lane < ne) {
+                jl = col[e0 + lane];
+                al = aval ? aval[e0 + lane] : 1.0f;
+            }
+            for (int u0 = 0; u0 < ne; u0 += 4) {
+                float v[4], a4[4];
+                int c[4];
+                int64_t jrow[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    jrow[u] = (int64_t)__shfl_sync(0xffffffffu, jl, (u0 + u) & 31) * ldv;
+                    a4[u] = __shfl_sync(0xffffffffu, al, (u0 + u) & 31);
+                    v[u] = 0.0f;
+                    c[u] = -1;
+                    if (u0 + u < ne && lane < k) {
+                        v[u] = vals[jrow[u] + lane];
+                        c[u] = fixed_col(idx, idx8, jrow[u] + lane);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if ((unsigned)c[u] < (unsigned)m)
+                        asm volatile("red.shared.add.f32 [%0], %1;" ::"r"(acc_base + 4u * c[u]), "f"(__fmul_rn(a4[u], v[u]))
+                                     : "memory");
+                // k > 32: the remaining entries of the same four rows, in the same edge order
+                for (int t = lane + 32; t < k; t += 32) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        if (u0 + u >= ne) break;
+                        const int cc = fixed_col(idx, idx8, jrow[u] + t);
+                        if ((unsigned)cc < (unsigned)m)
+                            asm volatile("red.shared.add.f32 [%0], %1;" ::"r"(acc_base + 4u * cc),
+                                         "f"(__fmul_rn(a4[u], vals[jrow[u] + t]))
+                                         : "memory");
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        float* orow = out + i * ldo;
+        for (int c = lane; c < m; c += 32) orow[c] = acc[c];
+        __syncwarp();
+    }
+}
+
+// Backward: one warp per row j of the fixed-k matrix, lane t owns entry t
+// and accumulates a_e * grad_out[i, idx[j, t]] over the in-edges of j in
+// registers (edge order, deterministic).
+__global__ void __launch_bounds__(kSpmmWarps * 32) maxk_spmm_backward_kernel(
+    const int64_t* __restrict__ rpt, const int32_t* __restrict__ colt, const float* __restrict__ avalt, int64_t n,
+    const float* __restrict__ gout, int64_t ldg, const int32_t* __restrict__ idx, const uint8_t* __restrict__ idx8,
+    int64_t ldv, int32_t k, int32_t m, float* __restrict__ gvals) {
+    const int lane = threadIdx.x & 31;
+    const int w = threadIdx.x >> 5;
+    const int64_t nw = (int64_t)gridDim.x * kSpmmWarps;
+    for (int64_t j = (int64_t)blockIdx.x * kSpmmWarps + w; j < n; j += nw) {
+        const int64_t e_beg = rpt[j], e_end = rpt[j + 1];
+        for (int t0 = 0; t0 < k; t0 += 32) {
+            const int t = t0 + lane;
+            const int cc = t < k ? fixed_col(idx, idx8, j * ldv + t) : 0;
+            const bool ok = t < k && (unsigned)cc < (unsigned)m;
+            float g = 0.0f;
+            for (int64_t e0 = e_beg; e0 < e_end; e0 += 32) {
+                const int ne = (int)((e_end - e0) < 32 ? (e_end - e0) : 32);
+                int il = 0;
+                float al = 0.0f;
+                if (lane < ne) {
+                    il = colt[e0 + lane];
+                    al = avalt ? avalt[e0 + lane] : 1.0f;
+                }
+                for (int u0 = 0; u0 < ne; u0 += 4) {  // four gathers in flight, summed in edge order
+                    float gv[4], a4[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int64_t ii = __shfl_sync(0xffffffffu, il, (u0 + u) & 31);
+                        a4[u] = __shfl_sync(0xffffffffu, al, (u0 + u) & 31);
+                        gv[u] = (ok && u0 + u < ne) ? gout[ii * ldg + cc] : 0.0f;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (u0 + u < ne) g = __fadd_rn(g, __fmul_rn(a4[u], gv[u]));
+                }
+            }
+            if (t < k) gvals[j * ldv + t] = g;
+        }
+    }
+}
+
 int grid_for(int64_t items, int per_cta, int cap_per_sm) {
     int64_t g = (items + per_cta - 1) / per_cta;
     const int64_t cap = (int64_t)rtk_device_sms() * cap_per_sm;
@@ -106,6 +238,37 @@ int rtk_gather_rows_f32(const float* dense, int64_t ldd, const int32_t* idx, int
         dense, ldd, idx, ldv, n, k, m, vals);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? RTK_OK : rtk_fail(RTK_ECUDA, "gather launch failed: %s", cudaGetErrorString(e));
+}
+
+int rtk_maxk_spmm_f32(const int64_t* row_ptr, const int32_t* col, const float* aval, int64_t n, const float* vals,
+                      const int32_t* idx, const uint8_t* idx8, int64_t ldv, int32_t k, int64_t m, float* out,
+                      int64_t ldo, void* stream) {
+    if (n < 0 || k < 1 || m < 1 || m > kSpmmMaxM || ldv < k || ldo < m)
+        return rtk_fail(RTK_EINVAL, "bad maxk_spmm shape (n=%lld, k=%d, m=%lld: m <= %d)", (long long)n, k,
+                        (long long)m, kSpmmMaxM);
+    if ((idx != nullptr) == (idx8 != nullptr)) return rtk_fail(RTK_EINVAL, "exactly one of idx / idx8 must be given");
+    if (idx8 && m > 256) return rtk_fail(RTK_EINVAL, "uint8 indices need m <= 256, got %lld", (long long)m);
+    if (n == 0) return RTK_OK;
+    if (!row_ptr || !col || !vals || !out) return rtk_fail(RTK_EINVAL, "NULL pointer");
+    maxk_spmm_kernel<<<grid_for(n, kSpmmWarps, 8), kSpmmWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(
+        row_ptr, col, aval, n, vals, idx, idx8, ldv, k, (int32_t)m, out, ldo);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? RTK_OK : rtk_fail(RTK_ECUDA, "maxk_spmm launch failed: %s", cudaGetErrorString(e));
+}
+
+int rtk_maxk_spmm_backward_f32(const int64_t* row_ptr_t, const int32_t* col_t, const float* aval_t, int64_t n,
+                               const float* grad_out, int64_t ldg, const int32_t* idx, const uint8_t* idx8,
+                               int64_t ldv, int32_t k, int64_t m, float* grad_vals, void* stream) {
+    if (n < 0 || k < 1 || m < 1 || ldv < k || ldg < m) return rtk_fail(RTK_EINVAL, "bad maxk_spmm_backward shape");
+    if ((idx != nullptr) == (idx8 != nullptr)) return rtk_fail(RTK_EINVAL, "exactly one of idx / idx8 must be given");
+    if (idx8 && m > 256) return rtk_fail(RTK_EINVAL, "uint8 indices need m <= 256, got %lld", (long long)m);
+    if (n == 0) return RTK_OK;
+    if (!row_ptr_t || !col_t || !grad_out || !grad_vals) return rtk_fail(RTK_EINVAL, "NULL pointer");
+    maxk_spmm_backward_kernel<<<grid_for(n, kSpmmWarps, 8), kSpmmWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(
+        row_ptr_t, col_t, aval_t, n, grad_out, ldg, idx, idx8, ldv, k, (int32_t)m, grad_vals);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? RTK_OK
+                            : rtk_fail(RTK_ECUDA, "maxk_spmm_backward launch failed: %s", cudaGetErrorString(e));
 }
 
 }  // extern "C"

@@ -179,7 +179,8 @@ __device__ __forceinline__ void finish_exact(const Row& row, const Args& a, int 
 // rtk_maxk_dense: after a row's selection (k indices staged at
 // sbase + kIdxOff by every path: select_flush_pair, finish_exact, row_body),
 // write the dense MaxK row -- x with all but the selected entries set to
-// +0 -- straight from the register tile: the staged indices set bits of a
+// +0 -- and / or a uint8 copy of the indices (the compact index layout of
+// the MaxK sparse rows for M <= 256), straight from the register tile: the staged indices set bits of a
 // 32E-bit shared bitmap (atomic OR), then each lane stores its E contiguous
 // elements (value or zero) with vector stores in the input type (16-bit
 // rows: the tile holds their exact fp32 widening, narrowed back exactly).
@@ -194,6 +195,15 @@ template <class In, class Row>
 __device__ __forceinline__ void dense_row(const Row& R, unsigned sbase, const Args& a, unsigned r, int lane) {
     constexpr int E = Row::kSlots;
     static_assert(E == 4 || E == 8, "fused MaxK rows: E = 4 or 8 (M = 128 or 256)");
+    if (a.idx8) {  // uint8 copy of the staged indices (M <= 256)
+        unsigned char* o8 = a.idx8 + (unsigned long long)r * (unsigned long long)a.ld8;
+        for (int j = lane; j < a.k; j += 32) {
+            unsigned i;
+            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(i) : "r"(sbase + Row::kIdxOff + 4u * j) : "memory");
+            o8[j] = (unsigned char)i;
+        }
+    }
+    if (!a.dense) return;
     const unsigned bm = sbase + Row::kStageBytes;
     if (lane < E) asm volatile("st.shared.b32 [%0], %1;" ::"r"(bm + 4u * lane), "r"(0u) : "memory");
     __syncwarp();

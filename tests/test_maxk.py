@@ -243,3 +243,78 @@ def test_maxk_dense_uses_fused_kernel_and_grads():
     g = torch.randn(n, m, device="cuda")
     (y * g).sum().backward()
     assert torch.equal(x.grad, torch.where(y != 0, g, torch.zeros((), device="cuda")))
+
+
+def _random_graph(n_out, n_in, g, max_deg=80):
+    deg = torch.randint(0, max_deg, (n_out,), device="cuda", generator=g)
+    deg[::97] = 0  # empty rows
+    deg[5] = 300   # several 32-edge chunks
+    row_ptr = torch.zeros(n_out + 1, dtype=torch.int64, device="cuda")
+    row_ptr[1:] = torch.cumsum(deg, 0)
+    nnz = int(row_ptr[-1])
+    col = torch.randint(0, n_in, (nnz,), device="cuda", generator=g, dtype=torch.int32)
+    aval = torch.rand(nnz, device="cuda", generator=g) + 0.5
+    return row_ptr, col, aval
+
+
+def _dense_adj(row_ptr, col, aval, n_in):
+    n_out = row_ptr.numel() - 1
+    rows = torch.repeat_interleave(torch.arange(n_out, device="cuda"), row_ptr[1:] - row_ptr[:-1])
+    a = torch.zeros(n_out, n_in, dtype=torch.float64, device="cuda")
+    a.index_put_((rows, col.long()), aval.double(), accumulate=True)
+    return a
+
+
+@pytest.mark.parametrize("m,k", [(256, 32), (128, 8), (256, 64), (700, 48), (1024, 128)])
+def test_maxk_spmm_forward_backward_against_float64(m, k):
+    """MaxK-GNN aggregation over the fixed-k rows: forward and the gradient
+    w.r.t. the kept values against float64 dense formulations (A @ scatter(H)
+    and (A^T @ grad)[j, idx[j]]), deterministic across calls, uint8 indices
+    equal to int32 ones (M <= 256), unit weights (aval = None)."""
+    g = torch.Generator(device="cuda").manual_seed(m * 31 + k)
+    n_in, n_out = 2500, 3000
+    h = torch.randn(n_in, m, device="cuda", generator=g)
+    res = rtk.batch_topk(h, rtk.BatchConfig(k=k))
+    vals, idx = res.values, res.indices
+    row_ptr, col, aval = _random_graph(n_out, n_in, g)
+    a = _dense_adj(row_ptr, col, aval, n_in)
+    hs = torch.zeros(n_in, m, dtype=torch.float64, device="cuda").scatter_(1, idx.long(), vals.double())
+    want = a @ hs
+    out = rtk.maxk_spmm(row_ptr, col, aval, vals, idx, m)
+    assert torch.allclose(out.double(), want, rtol=1e-5, atol=1e-4)
+    assert torch.equal(out, rtk.maxk_spmm(row_ptr, col, aval, vals, idx, m))  # deterministic
+    if m <= 256:
+        assert torch.equal(out, rtk.maxk_spmm(row_ptr, col, aval, vals, idx.to(torch.uint8), m))
+    ones = rtk.maxk_spmm(row_ptr, col, None, vals, idx, m)
+    a1 = _dense_adj(row_ptr, col, torch.ones_like(aval), n_in)
+    assert torch.allclose(ones.double(), a1 @ hs, rtol=1e-5, atol=1e-4)
+    # gradient w.r.t. the kept values
+    v = vals.clone().requires_grad_(True)
+    y = rtk.maxk_aggregate((row_ptr, col, aval), v, idx, m)
+    gout = torch.randn(n_out, m, device="cuda", generator=g)
+    (y * gout).sum().backward()
+    gref = torch.gather(a.t() @ gout.double(), 1, idx.long())
+    assert torch.allclose(v.grad.double(), gref, rtol=1e-5, atol=1e-4)
+    gt = rtk.csr_transpose(row_ptr, col, aval, n_in)
+    v2 = vals.clone().requires_grad_(True)
+    (rtk.maxk_aggregate((row_ptr, col, aval), v2, idx, m, graph_t=gt) * gout).sum().backward()
+    assert torch.equal(v2.grad, v.grad)
+
+
+def test_maxk_sparse_u8_and_spmm_errors():
+    x = torch.randn(513, 256, device="cuda")
+    vals, idx8 = rtk.maxk_sparse_u8(x, 32)
+    want = rtk.batch_topk(x, rtk.BatchConfig(k=32))
+    assert idx8.dtype == torch.uint8 and torch.equal(idx8.long(), want.indices.long())
+    assert torch.equal(vals, want.values)
+    v, i8 = rtk.maxk_sparse_u8(x[:, :128].contiguous(), 16, rtk.SearchConfig.early_stop(4))
+    w2 = rtk.batch_topk(x[:, :128].contiguous(), rtk.BatchConfig(k=16, search=rtk.SearchConfig.early_stop(4)))
+    assert torch.equal(i8.long(), w2.indices.long()) and torch.equal(v, w2.values)
+    rp = torch.tensor([0, 1], dtype=torch.int64, device="cuda")
+    c = torch.tensor([0], dtype=torch.int32, device="cuda")
+    with pytest.raises(rtk.DeviceError, match="m <= 256"):
+        rtk.maxk_spmm(rp, c, None, want.values, want.indices.to(torch.uint8), 300)
+    with pytest.raises(rtk.DeviceError, match="m <= 1024"):
+        rtk.maxk_spmm(rp, c, None, want.values, want.indices, 2000)
+    with pytest.raises(ValueError, match="int64"):
+        rtk.maxk_spmm(rp.int(), c, None, want.values, want.indices, 256)

@@ -57,6 +57,33 @@ def main():
         out["cases"].append(case)
         del x, dense
         torch.cuda.empty_cache()
+    # MaxK-GNN aggregation at the Reddit node count (synthetic uniform graph,
+    # mean degree 50): A @ MaxK(H) over the fixed-k rows vs cuSPARSE SpMM on
+    # the dense MaxK rows (torch.sparse.mm on a CSR tensor)
+    n, m, k, deg = 232965, 256, 32, 50
+    g = torch.Generator(device="cuda").manual_seed(0)
+    h = torch.randn(n, m, device="cuda", generator=g)
+    vals, idx = rtk.topk_device(h, k)
+    idx8 = idx.to(torch.uint8)
+    row_ptr = torch.arange(0, n * deg + 1, deg, dtype=torch.int64, device="cuda")
+    col = torch.randint(0, n, (n * deg,), device="cuda", generator=g, dtype=torch.int32)
+    aval = torch.rand(n * deg, device="cuda", generator=g)
+    hm = rtk.scatter_rows(vals, idx, m)
+    a_csr = torch.sparse_csr_tensor(row_ptr, col.to(torch.int64), aval, size=(n, n))  # one index dtype
+    t_u8 = t_ms(lambda: rtk.maxk_spmm(row_ptr, col, aval, vals, idx8, m), 20)
+    t_i32 = t_ms(lambda: rtk.maxk_spmm(row_ptr, col, aval, vals, idx, m), 20)
+    t_cus = t_ms(lambda: torch.sparse.mm(a_csr, hm), 10)
+    gt = rtk.csr_transpose(row_ptr, col, aval, n)
+    gout = torch.randn(n, m, device="cuda", generator=g)
+    gv = torch.empty_like(vals)
+    t_bw = t_ms(lambda: rtk._native.call("rtk_maxk_spmm_backward_f32", gt[0].data_ptr(), gt[1].data_ptr(),
+                                          gt[2].data_ptr(), n, gout.data_ptr(), m, idx.data_ptr(), None, k, k, m,
+                                          gv.data_ptr(), torch.cuda.current_stream().cuda_stream), 10)
+    nnz = n * deg
+    out["aggregation"] = {"N": n, "M": m, "k": k, "mean_degree": deg, "edges": nnz,
+                          "maxk_spmm_u8_ms": t_u8, "maxk_spmm_i32_ms": t_i32, "cusparse_dense_maxk_ms": t_cus,
+                          "speedup_u8_vs_cusparse": t_cus / t_u8, "backward_ms": t_bw,
+                          "edge_bytes_u8": nnz * (k * 5 + 8), "edge_bytes_dense": nnz * (m * 4 + 8)}
     print(json.dumps(out))
 
 
