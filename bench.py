@@ -415,14 +415,16 @@ def c5_leg(args, rank, world, local, peak, rtk):
         torch.cuda.synchronize()
         assert int(nan_word.item()) == -1
         cs = sum_u64(result_checksum(o[0], o[1], a), world)
-        ms_max, ms_mine = time_launches(lambda o=o, s=s: dm.launch_topk(k, s, False, outputs=o, nan_word=nan_word),
-                                        args.c5_steps, 3, world, stream)
+        with ClockSampler(local) as smp:
+            ms_max, ms_mine = time_launches(lambda o=o, s=s: dm.launch_topk(k, s, False, outputs=o, nan_word=nan_word),
+                                            args.c5_steps, 3, world, stream, smp)
+            clocks = smp.summary()
         per_rank = all_gather_floats(ms_mine, world)
         agg_gbs = n_tot * (4 * m + 8 * k) / (ms_max * 1e-3) / 1e9
         out[md] = {"ms_per_step": ms_max, "rows_per_s": n_tot / (ms_max * 1e-3), "gb_per_s": agg_gbs,
                    "frac_of_world_peak": agg_gbs / (world * peak), "per_rank_ms": per_rank,
                    "per_rank_gb_per_s": byts / (ms_mine * 1e-3) / 1e9, "steps": args.c5_steps,
-                   "checksum": f"{cs:016x}"}
+                   "checksum": f"{cs:016x}", "clocks": clocks}
         del o
     del x, dm
     torch.cuda.empty_cache()

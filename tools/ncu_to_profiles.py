@@ -25,6 +25,7 @@ CAPTURES = {  # capture -> (bench workload key, rows)
     "m2048_exact": ("custom 524288:2048:64:exact", 1 << 19),
     "m2048_early": ("custom 524288:2048:64:early", 1 << 19),
     "m8192_exact": ("custom 131072:8192:128:exact", 1 << 17),
+    "m512_exact": ("custom 1048576:512:64:exact", 1 << 20),
     "m128_exact": ("custom 1048576:128:32:exact", 1 << 20),
     "m128_early": ("custom 1048576:128:32:early", 1 << 20),
     "m768_exact": ("custom 1048576:768:64:exact", 1 << 20),
@@ -104,7 +105,7 @@ def main():
         tot = sum(sum(v) for v in agg.values())
         with open(os.path.join(prof, f"{tag}_launches.txt"), "w") as f:
             f.write("# ncu --metrics gpu__time_duration.sum --clock-control none -c 80: python bench.py --steps 10 "
-                    "--warmup 3 --no-cpu --no-e2e\n# (cold-cache, serialised replay: compare SHARES, not absolutes)\n")
+                    "--warmup 3 --no-cpu --no-e2e [--no-c5]\n# (cold-cache, serialised replay: compare SHARES, not absolutes)\n")
             f.write(f"{'launches':>8} {'mean us':>10} {'share':>7}  kernel\n")
             for name, v in agg.items():
                 f.write(f"{len(v):8d} {sum(v) / len(v) / 1e3:10.1f} {sum(v) / tot:7.1%}  {name}\n")
