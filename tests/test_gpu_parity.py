@@ -267,6 +267,12 @@ def test_single_row_helpers():
         rtk.min_max([])
     with pytest.raises(rtk.NaNInputError):
         rtk.min_max([1.0, float("nan")])
+    with pytest.raises(rtk.NaNInputError, match="row contains NaN"):
+        rtk.min_max([float("nan"), 2.0, float("inf")])
+    with pytest.raises(rtk.NaNInputError, match="row contains NaN"):  # NaN before the k range (select.py:97-112)
+        rtk.exact_topk([1.0, float("nan")], 5)
+    with pytest.raises(rtk.NaNInputError, match="row contains NaN"):
+        rtk.early_stop_topk([float("nan")] * 3, 1, rtk.SearchConfig.early_stop(2))
     with pytest.raises(rtk.NaNInputError):
         rtk.count_ge([1.0], float("nan"))
     with pytest.raises(rtk.KOutOfRangeError):
