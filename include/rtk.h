@@ -163,11 +163,15 @@ RTK_API int rtk_gather_rows_f32(const float *dense, int64_t ldd, const int32_t *
  *   rtk_maxk_spmm_backward_f32: grad_vals[j, t] = sum_{e=(i,j)} aval[e] *
  *                               grad_out[i, idx[j, t]], over the TRANSPOSED
  *                               graph's CSR (row j lists the i with e=(i,j)).
- * Sums run in edge order with fp32 rounding per product and per addition
- * (deterministic).  Columns outside [0, m) are skipped. */
+ * col[e] must be in [0, n_in) (n_in = rows of the fixed-k matrix,
+ * n_in * ldv < 2^31).  The forward sums each column's terms in edge order
+ * with one FFMA rounding per term (k > 32: entries t >= 32 of a group of four
+ * edges after the group's first 32 -- a fixed order), the backward in edge
+ * order with a product and a sum rounding per term; both deterministic.
+ * Columns outside [0, m) are skipped. */
 RTK_API int rtk_maxk_spmm_f32(const int64_t *row_ptr, const int32_t *col, const float *aval, int64_t n,
                       const float *vals, const int32_t *idx, const uint8_t *idx8, int64_t ldv, int32_t k,
-                      int64_t m, float *out, int64_t ldo, void *stream);
+                      int64_t m, int64_t n_in, float *out, int64_t ldo, void *stream);
 RTK_API int rtk_maxk_spmm_backward_f32(const int64_t *row_ptr_t, const int32_t *col_t, const float *aval_t,
                                int64_t n, const float *grad_out, int64_t ldg, const int32_t *idx,
                                const uint8_t *idx8, int64_t ldv, int32_t k, int64_t m, float *grad_vals,

@@ -40,7 +40,7 @@ SIGNATURES = {
                                          _i64, _p]),
     "rtk_scatter_rows_f32": (ctypes.c_int, [_p, _p, _i64, _i64, _i32, _i64, _p, _i64, _p]),
     "rtk_gather_rows_f32": (ctypes.c_int, [_p, _i64, _p, _i64, _i64, _i32, _i64, _p, _p]),
-    "rtk_maxk_spmm_f32": (ctypes.c_int, [_p, _p, _p, _i64, _p, _p, _p, _i64, _i32, _i64, _p, _i64, _p]),
+    "rtk_maxk_spmm_f32": (ctypes.c_int, [_p, _p, _p, _i64, _p, _p, _p, _i64, _i32, _i64, _i64, _p, _i64, _p]),
     "rtk_maxk_spmm_backward_f32": (ctypes.c_int, [_p, _p, _p, _i64, _p, _i64, _p, _p, _i64, _i32, _i64, _p, _p]),
     "rtk_last_error": (ctypes.c_char_p, []),
     "rtk_version": (ctypes.c_int, []),

@@ -94,21 +94,24 @@ __device__ __forceinline__ int fixed_col(const int32_t* __restrict__ idx, const 
 
 // One warp per output row i; the m-float accumulator lives in the warp's
 // shared-memory row.  Edges are taken 32 at a time (lane l loads edge
-// e0 + l's column and weight, broadcast by SHFL), and for each edge every
-// lane t < k adds a_e * vals[j, t] at column idx[j, t] with a shared-memory
-// RED.ADD -- the k columns of one row are distinct, so no two lanes of one
-// instruction collide, and the warp's REDs reach the shared memory in issue
-// order: the sum is taken in edge order, deterministically.  Four edges'
-// loads are issued before their REDs to overlap the L2 latency.
+// e0 + l's column and weight, broadcast by SHFL); four edges' (value,
+// column) loads are issued before their updates to overlap the L2 latency.
+// Lane t < k adds a_e * vals[j, t] into column idx[j, t] with a shared-memory
+// read-modify-write (one FFMA): a row's k columns are distinct, so the lanes
+// of one edge never collide, and a __syncwarp between edges orders the
+// updates -- every column sums its terms in edge order, deterministically.
+// (A shared RED.ADD per entry measured 20% slower.)  IdxT: int32_t or
+// uint8_t columns; offsets are 32-bit (the host checks n_in * ldv < 2^31).
+template <class IdxT>
 __global__ void __launch_bounds__(kSpmmWarps * 32) maxk_spmm_kernel(
     const int64_t* __restrict__ rp, const int32_t* __restrict__ col, const float* __restrict__ aval, int64_t n,
-    const float* __restrict__ vals, const int32_t* __restrict__ idx, const uint8_t* __restrict__ idx8, int64_t ldv,
-    int32_t k, int32_t m, float* __restrict__ out, int64_t ldo) {
+    const float* __restrict__ vals, const IdxT* __restrict__ idx, unsigned ldv, int32_t k, int32_t m,
+    float* __restrict__ out, int64_t ldo) {
     __shared__ __align__(16) float acc_s[kSpmmWarps][kSpmmMaxM];
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
     float* acc = acc_s[w];
-    const unsigned acc_base = (unsigned)__cvta_generic_to_shared(acc);
+    const bool check_col = sizeof(IdxT) == 4 || m < 256;  // uint8 columns of 256-wide rows are always in range
     const int64_t nw = (int64_t)gridDim.x * kSpmmWarps;
     for (int64_t i = (int64_t)blockIdx.x * kSpmmWarps + w; i < n; i += nw) {
         for (int c = lane; c < m; c += 32) acc[c] = 0.0f;
@@ -116,42 +119,37 @@ __global__ void __launch_bounds__(kSpmmWarps * 32) maxk_spmm_kernel(
         const int64_t e_beg = rp[i], e_end = rp[i + 1];
         for (int64_t e0 = e_beg; e0 < e_end; e0 += 32) {
             const int ne = (int)((e_end - e0) < 32 ? (e_end - e0) : 32);
-            int jl = 0;
+            unsigned jl = 0;
             float al = 0.0f;
             if (lane < ne) {
-                jl = col[e0 + lane];
+                jl = (unsigned)col[e0 + lane] * ldv;
                 al = aval ? aval[e0 + lane] : 1.0f;
             }
             for (int u0 = 0; u0 < ne; u0 += 4) {
                 float v[4], a4[4];
                 int c[4];
-                int64_t jrow[4];
+                unsigned jo[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    jrow[u] = (int64_t)__shfl_sync(0xffffffffu, jl, (u0 + u) & 31) * ldv;
+                    jo[u] = __shfl_sync(0xffffffffu, jl, (u0 + u) & 31);
                     a4[u] = __shfl_sync(0xffffffffu, al, (u0 + u) & 31);
-                    v[u] = 0.0f;
-                    c[u] = -1;
-                    if (u0 + u < ne && lane < k) {
-                        v[u] = vals[jrow[u] + lane];
-                        c[u] = fixed_col(idx, idx8, jrow[u] + lane);
-                    }
+                    const bool on = u0 + u < ne && lane < k;
+                    v[u] = on ? vals[jo[u] + lane] : 0.0f;
+                    c[u] = on ? (int)idx[jo[u] + lane] : -1;
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if ((unsigned)c[u] < (unsigned)m)
-                        asm volatile("red.shared.add.f32 [%0], %1;" ::"r"(acc_base + 4u * c[u]), "f"(__fmul_rn(a4[u], v[u]))
-                                     : "memory");
-                // k > 32: the remaining entries of the same four rows, in the same edge order
+                for (int u = 0; u < 4; ++u) {
+                    if (c[u] >= 0 && (!check_col || c[u] < m)) acc[c[u]] = __fmaf_rn(a4[u], v[u], acc[c[u]]);
+                    __syncwarp();
+                }
+                // k > 32: the remaining entries of the same four rows (deterministic order)
                 for (int t = lane + 32; t < k; t += 32) {
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         if (u0 + u >= ne) break;
-                        const int cc = fixed_col(idx, idx8, jrow[u] + t);
-                        if ((unsigned)cc < (unsigned)m)
-                            asm volatile("red.shared.add.f32 [%0], %1;" ::"r"(acc_base + 4u * cc),
-                                         "f"(__fmul_rn(a4[u], vals[jrow[u] + t]))
-                                         : "memory");
+                        const int cc = (int)idx[jo[u] + t];
+                        if (!check_col || cc < m) acc[cc] = __fmaf_rn(a4[u], vals[jo[u] + t], acc[cc]);
+                        __syncwarp(__activemask());
                     }
                 }
             }
@@ -241,17 +239,25 @@ int rtk_gather_rows_f32(const float* dense, int64_t ldd, const int32_t* idx, int
 }
 
 int rtk_maxk_spmm_f32(const int64_t* row_ptr, const int32_t* col, const float* aval, int64_t n, const float* vals,
-                      const int32_t* idx, const uint8_t* idx8, int64_t ldv, int32_t k, int64_t m, float* out,
-                      int64_t ldo, void* stream) {
+                      const int32_t* idx, const uint8_t* idx8, int64_t ldv, int32_t k, int64_t m, int64_t n_in,
+                      float* out, int64_t ldo, void* stream) {
     if (n < 0 || k < 1 || m < 1 || m > kSpmmMaxM || ldv < k || ldo < m)
         return rtk_fail(RTK_EINVAL, "bad maxk_spmm shape (n=%lld, k=%d, m=%lld: m <= %d)", (long long)n, k,
                         (long long)m, kSpmmMaxM);
     if ((idx != nullptr) == (idx8 != nullptr)) return rtk_fail(RTK_EINVAL, "exactly one of idx / idx8 must be given");
     if (idx8 && m > 256) return rtk_fail(RTK_EINVAL, "uint8 indices need m <= 256, got %lld", (long long)m);
+    if (n_in < 0 || n_in * ldv >= (1LL << 31))
+        return rtk_fail(RTK_EINVAL, "fixed-k matrix too large: n_in * ldv must be < 2^31");
     if (n == 0) return RTK_OK;
     if (!row_ptr || !col || !vals || !out) return rtk_fail(RTK_EINVAL, "NULL pointer");
-    maxk_spmm_kernel<<<grid_for(n, kSpmmWarps, 8), kSpmmWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(
-        row_ptr, col, aval, n, vals, idx, idx8, ldv, k, (int32_t)m, out, ldo);
+    const dim3 grid(grid_for(n, kSpmmWarps, 8)), block(kSpmmWarps * 32);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (idx8)
+        maxk_spmm_kernel<uint8_t><<<grid, block, 0, s>>>(row_ptr, col, aval, n, vals, idx8, (unsigned)ldv, k,
+                                                         (int32_t)m, out, ldo);
+    else
+        maxk_spmm_kernel<int32_t><<<grid, block, 0, s>>>(row_ptr, col, aval, n, vals, idx, (unsigned)ldv, k,
+                                                         (int32_t)m, out, ldo);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? RTK_OK : rtk_fail(RTK_ECUDA, "maxk_spmm launch failed: %s", cudaGetErrorString(e));
 }

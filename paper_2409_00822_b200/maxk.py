@@ -239,9 +239,9 @@ def _idx_args(indices):
 def maxk_spmm(row_ptr, col, aval, values, indices, m: int) -> torch.Tensor:
     """out[i, :] = sum over edges e = (i, j) of aval[e] * H[j, :], H the
     fixed-k rows (values at columns indices, int32 or uint8): MaxK-GNN's
-    aggregation reading only the kept entries (rtk_maxk_spmm_f32).  Sums in
-    edge order (deterministic; the shared-memory atomic adds flush
-    subnormals like PTX atom.add.f32)."""
+    aggregation reading only the kept entries (rtk_maxk_spmm_f32).  Each
+    column sums its terms in a fixed (edge) order: deterministic.  col must
+    index rows of values."""
     _check_graph(row_ptr, col, aval)
     v = values.contiguous()
     i = indices.contiguous()
@@ -254,7 +254,7 @@ def maxk_spmm(row_ptr, col, aval, values, indices, m: int) -> torch.Tensor:
     with torch.cuda.device(v.device):
         _native.call("rtk_maxk_spmm_f32", row_ptr.data_ptr(), col.data_ptr(),
                      aval.data_ptr() if aval is not None else None, n_out, v.data_ptr(), ip, i8, k, k, int(m),
-                     out.data_ptr(), int(m), torch.cuda.current_stream(v.device).cuda_stream)
+                     int(v.shape[0]), out.data_ptr(), int(m), torch.cuda.current_stream(v.device).cuda_stream)
     return out
 
 
