@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(kSpmmWarps * 32) maxk_spmm_kernel(
                         __syncwarp(__activemask());
                     }
                 }
+                __syncwarp();  // lanes that skipped the loop above wait for its updates (racecheck)
             }
         }
         __syncwarp();

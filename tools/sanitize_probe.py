@@ -1,7 +1,8 @@
 """Small launches of every kernel family under compute-sanitizer: paired-row
 (E=4, 8; masked/unmasked; odd N), long-row (E=12..32), general kernels
 (traces, RegRow, GlobalRow), k == M, NaN rows, the host pipeline, the file
-job and the MaxK scatter/gather.  Exits non-zero on a parity mismatch."""
+job, the MaxK scatter/gather, the fused MaxK rows and the aggregation.
+Exits non-zero on a parity mismatch."""
 import os
 import sys
 import tempfile
@@ -47,6 +48,26 @@ def main():
     res = rtk.batch_topk(xd, rtk.BatchConfig(k=32))
     d = rtk.scatter_rows(res.values, res.indices, 256)
     assert torch.equal(rtk.gather_rows(d, res.indices), res.values)
+    # fused MaxK rows (dense + uint8 indices) and the aggregation kernels
+    for dt in (torch.float32, torch.bfloat16):
+        for m in (128, 256):
+            xs = torch.randn(67, m, device="cuda").to(dt)
+            xs[3] = 1.0
+            for search in (rtk.SearchConfig.exact(), rtk.SearchConfig.early_stop(3)):
+                dense, vals, idx = rtk.maxk_dense_fused(xs, 9, search)
+                v8, i8 = rtk.maxk_sparse_u8(xs, 9, search)
+                assert torch.equal(i8.long(), idx.long()) and torch.equal(v8, vals)
+                assert torch.equal(dense, rtk.scatter_rows(vals, idx, m).to(dt))
+    hv = torch.randn(300, 256, device="cuda")
+    tv, ti = rtk.topk_device(hv, 40)
+    rp = torch.tensor([0, 0, 3, 40, 41, 120], dtype=torch.int64, device="cuda")
+    cl = torch.randint(0, 300, (120,), dtype=torch.int32, device="cuda")
+    av = torch.rand(120, device="cuda")
+    o1 = rtk.maxk_spmm(rp, cl, av, tv, ti, 256)
+    o2 = rtk.maxk_spmm(rp, cl, av, tv, ti.to(torch.uint8), 256)
+    assert torch.equal(o1, o2)
+    vv = tv.clone().requires_grad_(True)
+    rtk.maxk_aggregate((rp, cl, av), vv, ti, 256).sum().backward()
     with tempfile.TemporaryDirectory() as tdir:
         p, q = os.path.join(tdir, "x.rtkm"), os.path.join(tdir, "o.rtkr")
         rtk.save_matrix(rng.standard_normal((3000, 96), dtype=np.float32), p)
