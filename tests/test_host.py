@@ -61,6 +61,25 @@ def test_cabi_rejects_bad_arguments_without_touching_the_gpu(lib):
     assert lib.rtk_launch_shape(8, 9, 0, None, None, None) == 1
     # n == 0 is a no-op
     assert lib.rtk_rowtopk_exact_f32(None, 0, 8, 8, 2, 0.0, 64, None, None, 2, None, None, None, None) == 0
+    # fused MaxK rows: dtype, outputs, native-path shape (RTK_EUNSUPPORTED = 7)
+    assert lib.rtk_maxk_dense(fake, 3, 0, 4, 256, 256, 8, 64, 4, fake, fake, 8, fake, 256, None, 0, None, None) == 1
+    assert b"dtype" in lib.rtk_last_error()
+    assert lib.rtk_maxk_dense(fake, 0, 0, 4, 256, 256, 8, 64, 4, fake, fake, 8, None, 0, None, 0, None, None) == 1
+    assert b"both NULL" in lib.rtk_last_error()
+    assert lib.rtk_maxk_dense(fake, 0, 0, 4, 256, 256, 300, 64, 4, fake, fake, 300, fake, 256, None, 0, None,
+                              None) == 1
+    assert lib.rtk_maxk_dense(fake, 0, 0, 4, 200, 200, 8, 64, 4, fake, fake, 8, fake, 200, None, 0, None, None) == 7
+    assert b"fused MaxK path" in lib.rtk_last_error()
+    # aggregation: exactly one index array, width limits, 32-bit offsets
+    assert lib.rtk_maxk_spmm_f32(fake, fake, None, 4, fake, fake, fake, 32, 32, 256, 10, fake, 256, None) == 1
+    assert b"exactly one of idx / idx8" in lib.rtk_last_error()
+    assert lib.rtk_maxk_spmm_f32(fake, fake, None, 4, fake, None, fake, 32, 32, 300, 10, fake, 300, None) == 1
+    assert b"m <= 256" in lib.rtk_last_error()
+    assert lib.rtk_maxk_spmm_f32(fake, fake, None, 4, fake, fake, None, 32, 32, 2000, 10, fake, 2000, None) == 1
+    assert lib.rtk_maxk_spmm_f32(fake, fake, None, 4, fake, fake, None, 32, 32, 256, 1 << 27, fake, 256, None) == 1
+    assert b"2^31" in lib.rtk_last_error()
+    assert lib.rtk_maxk_spmm_backward_f32(fake, fake, None, 4, fake, 100, fake, None, 32, 32, 256, fake, None) == 1
+    assert lib.rtk_maxk_spmm_f32(None, None, None, 0, None, fake, None, 32, 32, 256, 0, None, 256, None) == 0
 
 
 def test_search_config_validation_mirrors_reference():
