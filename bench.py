@@ -220,11 +220,17 @@ def maybe_spawn(args) -> None:
     import torch
 
     have = torch.cuda.device_count()
-    if have < args.gpus:
+    if have < args.gpus and not SHARED_GPU:
         sys.exit(f"bench.py: --gpus {args.gpus} needs {args.gpus} CUDA devices, this node has {have}")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
     sys.exit(subprocess.call(cmd))
+
+
+# Harness test mode (tests of the multi-rank path on a 1-GPU box): every rank
+# uses cuda:0 and the process group runs over gloo with host tensors.  Never
+# used for reported numbers.
+SHARED_GPU = os.environ.get("RTK_BENCH_SHARED_GPU") == "1"
 
 
 def dist_setup():
@@ -236,11 +242,20 @@ def dist_setup():
     if world > 1:
         import torch.distributed as dist
 
+        if SHARED_GPU:
+            local = 0
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+            return rank, world, local
         if local >= torch.cuda.device_count():
             sys.exit(f"bench.py: rank {rank} needs cuda:{local}, this node has {torch.cuda.device_count()} devices")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
+
+
+def _coll_device():
+    return "cpu" if SHARED_GPU else "cuda"
 
 
 def reduce_max(x, world):
@@ -249,7 +264,7 @@ def reduce_max(x, world):
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=_coll_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -260,7 +275,7 @@ def all_gather_floats(x, world):
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=_coll_device())
     parts = [torch.empty_like(t) for _ in range(world)]
     dist.all_gather(parts, t)
     return [float(p.item()) for p in parts]

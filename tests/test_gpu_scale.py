@@ -188,3 +188,30 @@ def test_two_ranks_on_one_gpu_gather_equals_unsharded():
             fv, fi, li = got[rank][mode]
             assert np.array_equal(fi, wi) and np.array_equal(_u32(fv), _u32(wv)), (mode, rank)
             assert np.array_equal(li, wi), (mode, rank)
+
+
+def test_bench_two_ranks_harness_on_one_gpu():
+    """bench.py --gpus 2 end to end (self-spawn under torch.distributed.run,
+    barrier + max-over-ranks timing, the C5 strong-sharded leg) with both
+    ranks sharing cuda:0 over gloo (RTK_BENCH_SHARED_GPU, a harness test
+    mode): one JSON line with n_gpus = 2, the C2 digests checked in the run,
+    and C5 checksums equal to the 1-GPU run's (row sharding does not change
+    any output)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, RTK_BENCH_SHARED_GPU="1")
+    p = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "3", "--warmup", "3",
+                        "--no-cpu", "--no-torch", "--no-e2e", "--c5-steps", "2"],
+                       capture_output=True, text=True, env=env, timeout=900, cwd=root)
+    assert p.returncode == 0, p.stderr[-3000:]
+    line = json.loads(p.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["config"]["parallelism"] == "row shards x2 (no collective)"
+    assert line["parity"]["exact"]["ok"] and line["parity"]["early"]["ok"]
+    assert abs(line["value"] - 2 * (1 << 20) / (line["ms_per_step"] * 1e-3)) / line["value"] < 1e-9
+    assert line["c5"]["exact"]["checksum"] == "1d0d6250a151e306"
+    assert line["c5"]["early"]["checksum"] == "b601101e12c9fb17"
+    assert len(line["c5"]["exact"]["per_rank_ms"]) == 2
