@@ -13,6 +13,7 @@
 #pragma once
 
 #include "rtk_kernels.cuh"
+#include "rtk_pair.cuh"
 
 namespace rtk {
 
@@ -203,6 +204,78 @@ __global__ void __launch_bounds__(RTK_BIG_THREADS, BigMinCtas<E, false>::value)
         });
         if (rn >= n) break;
         r = (unsigned)rn;
+    }
+}
+
+// Paired long rows (E = 16, unmasked; exact with eps_rel = 0 or early stop,
+// no traces): the row-pair scheme of rtk_pair.cuh (both rows' bisection steps
+// interleaved, one FADD2 + FMUL2 for both midpoints, one f32x2 count tree)
+// on tiles fed by TMA: each warp owns two swizzled row slots and one
+// mbarrier; once both tiles are in registers (after the lane min/max) one
+// elected lane issues the next pair's two tensor copies.
+#ifndef RTK_BIG_PAIR
+#define RTK_BIG_PAIR 1
+#endif
+__device__ __forceinline__ void tma_row_noarrive(unsigned slot, const CUtensorMap* map, int row, unsigned bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(slot),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(0), "r"(0), "r"(row), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tma_pair(unsigned slotA, unsigned slotB, const CUtensorMap* map, int rowA, int rowB,
+                                         unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2u * bytes) : "memory");
+    tma_row_noarrive(slotA, map, rowA, bar);
+    tma_row_noarrive(slotB, map, rowB, bar);
+}
+
+template <int MODE, int E>
+__global__ void __launch_bounds__(RTK_BIG_THREADS, 4) rowtopk_big_pair_tma_kernel(Args a,
+                                                                                const __grid_constant__ CUtensorMap map) {
+    using Row = TmaRow<E>;
+    extern __shared__ __align__(16) float smem[];
+    const int lane = threadIdx.x & 31;
+    const int wid = __shfl_sync(kFull, (int)(threadIdx.x >> 5), 0);
+    const unsigned wpc = blockDim.x >> 5;
+    const unsigned base = (unsigned)__cvta_generic_to_shared(smem);
+    const unsigned stage_bytes = Row::stage_bytes(a.k);
+    const unsigned sA = base + (unsigned)wid * 2u * stage_bytes;
+    const unsigned sB = sA + stage_bytes;
+    const unsigned slots = (base + wpc * 2u * stage_bytes + Row::kSlotAlign - 1) & ~(Row::kSlotAlign - 1);
+    const unsigned slotA = slots + (unsigned)wid * 2u * Row::kSlotBytes;
+    const unsigned slotB = slotA + Row::kSlotBytes;
+    const unsigned bar = slots + wpc * 2u * Row::kSlotBytes + 8u * (unsigned)wid;
+    const unsigned nw = gridDim.x * wpc;
+    const unsigned n = (unsigned)a.n;  // the host guarantees n + 2 nw < 2^31
+    unsigned r = blockIdx.x * wpc + (unsigned)wid;
+    if (r >= n) return;
+    const unsigned last = n - 1;
+    const int steps = MODE == kEarly ? a.max_iter : min(a.hard_cap, RTK_FAST_STEPS);
+    if (lane == 0) {
+        mbar_init(bar);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        tma_pair(slotA, slotB, &map, (int)r, (int)min(r + nw, last), bar, Row::kSlotBytes);
+    }
+    __syncwarp();
+    unsigned phase = 0;
+    Row A, B;
+    for (;;) {
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        A.load_swizzled(slotA, lane);
+        B.load_swizzled(slotB, lane);
+        const unsigned rn = r + 2u * nw;
+        process_pair<MODE, false, float>(A, B, r, r + nw, r + nw < n, a, lane, sA, sB, steps, [&](unsigned tok) {
+            __syncwarp();  // every lane has read both slots
+            if (lane == 0 && rn < n) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                tma_pair(slotA, slotB, &map, (int)(rn + (tok & a.opaque_zero)), (int)min(rn + nw, last), bar,
+                         Row::kSlotBytes);
+            }
+        });
+        if (rn >= n) break;
+        r = rn;
     }
 }
 

@@ -135,11 +135,38 @@ int launch_big_tma_kernel(const rtk::Args& a, cudaStream_t s, const CUtensorMap&
     return RTK_OK;
 }
 
+// Paired long rows on TMA slots (rtk_big.cuh): E = 16, no traces, exact
+// with eps_rel = 0 or early stop.
+template <int MODE, int E>
+int launch_big_pair_tma_kernel(const rtk::Args& a, cudaStream_t s, const CUtensorMap& map) {
+    using Row = rtk::TmaRow<E>;
+    constexpr int wpc = RTK_BIG_THREADS / 32;
+    const size_t smem =
+        (size_t)wpc * 2 * Row::stage_bytes(a.k) + Row::kSlotAlign + (size_t)wpc * (2 * Row::kSlotBytes + 8);
+    auto kernel = rtk::rowtopk_big_pair_tma_kernel<MODE, E>;
+    if (describe(reinterpret_cast<const void*>(kernel), smem, RTK_BIG_THREADS, 2)) return RTK_OK;
+    const long long blocks_needed = (a.n + 2 * wpc - 1) / (2 * wpc);
+    long long grid = (long long)rtk_device_sms() * rtk_ctas_per_sm(reinterpret_cast<const void*>(kernel), smem,
+                                                                   RTK_BIG_THREADS);
+    if (grid > blocks_needed) grid = blocks_needed;
+    if (grid < 1) grid = 1;
+    kernel<<<(unsigned)grid, RTK_BIG_THREADS, smem, s>>>(a, map);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(RTK_ECUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+    return RTK_OK;
+}
+
 template <int MODE, int E, bool MASKED>
 int launch_big(const rtk::Args& a, cudaStream_t s) {
     if constexpr (RTK_USE_TMA && !MASKED && (E == 16 || E == 32)) {
         CUtensorMap map;
         if (a.n < (1LL << 31) && rtk_encode_row_map(&map, a.x, a.n, E, a.ldx)) {
+            if constexpr (RTK_BIG_PAIR && E == 16 && MODE != rtk::kTrace) {
+                // early stop with k >= 128 measured 6% slower paired (two k-pair flushes per step)
+                if (a.iters == nullptr && a.reasons == nullptr && a.n < (1LL << 30) &&
+                    (MODE == rtk::kEarly ? a.k < 128 : a.eps_rel == 0.0))
+                    return launch_big_pair_tma_kernel<MODE, E>(a, s, map);
+            }
             if constexpr (MODE == rtk::kTrace) {
                 return launch_big_tma_kernel<MODE, E, true>(a, s, map);
             } else {

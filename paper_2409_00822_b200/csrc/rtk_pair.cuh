@@ -154,6 +154,24 @@ __device__ __forceinline__ void select_flush_pair(const Row& A, const Row& B, fl
     __syncwarp();
 }
 
+// Selection of both rows at thresholds tA, tB (biased lane hits hA, hB):
+// LaneRow tiles share one packed scan and the row-copy flush
+// (select_flush_pair); the long-row tiles (LaneRowCut, paired TMA kernel)
+// stage each row's first k pairs and flush them.
+template <class Row>
+__device__ __forceinline__ void select_two(const Row& A, const Row& B, float tA, float tB, int hA, int hB, unsigned sA,
+                                           unsigned sB, int lane, int k, float* __restrict__ ovA, int* __restrict__ oiA,
+                                           float* __restrict__ ovB, int* __restrict__ oiB, bool vec4, unsigned oz) {
+    if constexpr (Row::kPad > 0) {
+        select_flush_pair(A, B, tA, tB, hA, hB, sA, sB, lane, k, ovA, oiA, ovB, oiB, vec4);
+    } else {
+        const unsigned dA = A.select_ge(tA, k, sA, lane, hA - (int)kLaneBias);
+        const unsigned dB = B.select_ge(tB, k, sB, lane, hB - (int)kLaneBias);
+        flush_staged<Row>(sA, k, ovA, oiA, lane, dA & oz);
+        flush_staged<Row>(sB, k, ovB, oiB, lane, dB & oz);
+    }
+}
+
 // Exact mode, one row after its fast loop ended (eq: cnt == k at mid).
 template <class Row>
 __device__ __forceinline__ void finish_exact(const Row& row, const Args& a, int lane, unsigned sbase, bool eq,
@@ -303,7 +321,7 @@ __device__ __forceinline__ void process_pair_sel(const Row& A, const Row& B, uns
         }
         // first k indices with v >= mn (_kernels.py:205-212)
         // (scalar flush: the vectorised one measured 2% slower in early-stop mode)
-        select_flush_pair(A, B, mnA, mnB, hA, hB, sA, sB, lane, k, ovA, oiA, ovB, oiB, false);
+        select_two(A, B, mnA, mnB, hA, hB, sA, sB, lane, k, ovA, oiA, ovB, oiB, false, a.opaque_zero);
     } else {
         // Algorithm 1 fast steps (exact_loop_fast) on both rows until either
         // meets cnt == k; the other continues alone.
@@ -329,7 +347,7 @@ __device__ __forceinline__ void process_pair_sel(const Row& A, const Row& B, uns
         if (!eqA && itA < steps) eqA = exact_loop_fast(A, kb, steps, mnA, mxA, midA, cA, itA, lA);
         if (!eqB && itB < steps) eqB = exact_loop_fast(B, kb, steps, mnB, mxB, midB, cB, itB, lB);
         if (eqA && eqB) {
-            select_flush_pair(A, B, midA, midB, lA, lB, sA, sB, lane, k, ovA, oiA, ovB, oiB, a.out_vec4 != 0);
+            select_two(A, B, midA, midB, lA, lB, sA, sB, lane, k, ovA, oiA, ovB, oiB, a.out_vec4 != 0, a.opaque_zero);
         } else {
             finish_exact(A, a, lane, sA, eqA, mnA, mxA, midA, cA, itA, lA, ovA, oiA);
             finish_exact(B, a, lane, sB, eqB, mnB, mxB, midB, cB, itB, lB, ovB, oiB);
