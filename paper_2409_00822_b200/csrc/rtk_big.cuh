@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(RTK_BIG_THREADS, BigMinCtas<E, false>::value)
     }
 }
 
-// Paired long rows (E = 16, unmasked; exact with eps_rel = 0 or early stop,
+// Paired long rows (E = 16 or 32: M = 512 / 1024, unmasked; exact with eps_rel = 0 or early stop,
 // no traces): the row-pair scheme of rtk_pair.cuh (both rows' bisection steps
 // interleaved, one FADD2 + FMUL2 for both midpoints, one f32x2 count tree)
 // on tiles fed by TMA: each warp owns two swizzled row slots and one
@@ -230,8 +230,13 @@ __device__ __forceinline__ void tma_pair(unsigned slotA, unsigned slotB, const C
     tma_row_noarrive(slotB, map, rowB, bar);
 }
 
+template <int E>
+struct BigPairMinCtas {  // E = 16: 64 registers (4 CTAs of 8 warps); E = 32: two 32-float tiles need ~100
+    static constexpr int value = E <= 16 ? 4 : 2;
+};
+
 template <int MODE, int E>
-__global__ void __launch_bounds__(RTK_BIG_THREADS, 4) rowtopk_big_pair_tma_kernel(Args a,
+__global__ void __launch_bounds__(RTK_BIG_THREADS, BigPairMinCtas<E>::value) rowtopk_big_pair_tma_kernel(Args a,
                                                                                 const __grid_constant__ CUtensorMap map) {
     using Row = TmaRow<E>;
     extern __shared__ __align__(16) float smem[];

@@ -161,7 +161,10 @@ int launch_big(const rtk::Args& a, cudaStream_t s) {
     if constexpr (RTK_USE_TMA && !MASKED && (E == 16 || E == 32)) {
         CUtensorMap map;
         if (a.n < (1LL << 31) && rtk_encode_row_map(&map, a.x, a.n, E, a.ldx)) {
-            if constexpr (RTK_BIG_PAIR && E == 16 && MODE != rtk::kTrace) {
+#ifndef RTK_BIG_PAIR_E32
+#define RTK_BIG_PAIR_E32 1
+#endif
+            if constexpr (RTK_BIG_PAIR && (E == 16 || (RTK_BIG_PAIR_E32 && E == 32)) && MODE != rtk::kTrace) {
                 // early stop with k >= 128 measured 6% slower paired (two k-pair flushes per step)
                 if (a.iters == nullptr && a.reasons == nullptr && a.n < (1LL << 30) &&
                     (MODE == rtk::kEarly ? a.k < 128 : a.eps_rel == 0.0))
