@@ -108,6 +108,65 @@ __global__ void __launch_bounds__(BigThreads<E>::value, BigMinCtas<E, MASKED>::v
     cp_async_wait<0>();
 }
 
+// Paired long rows through the cp.async ring (E = 12..32 incl. masked rows,
+// where the TMA map does not apply): two ring slots per warp, refilled with
+// the next pair once both tiles are in registers; same pair scheme as above.
+template <int E>
+struct BigPairCpMinCtas {
+    static constexpr int value = E <= 16 ? 4 : 2;
+};
+
+template <int MODE, int E, bool MASKED>
+__global__ void __launch_bounds__(RTK_BIG_THREADS, BigPairCpMinCtas<E>::value) rowtopk_big_pair_kernel(Args a) {
+    using Row = LaneRowCut<E, MASKED>;
+    constexpr unsigned kSlot = Row::kRowBytes;
+    extern __shared__ __align__(16) float smem[];
+    const int lane = threadIdx.x & 31;
+    const int wid = __shfl_sync(kFull, (int)(threadIdx.x >> 5), 0);
+    const unsigned wpc = blockDim.x >> 5;
+    const unsigned base = (unsigned)__cvta_generic_to_shared(smem);
+    const unsigned stage_bytes = Row::stage_bytes(a.k);
+    const unsigned sA = base + (unsigned)wid * 2u * stage_bytes;
+    const unsigned sB = sA + stage_bytes;
+    const unsigned ringA = base + wpc * 2u * stage_bytes + (unsigned)wid * 2u * kSlot;
+    const unsigned ringB = ringA + kSlot;
+    const unsigned nw = gridDim.x * wpc;
+    const unsigned n = (unsigned)a.n;  // the host guarantees n + 2 nw < 2^31
+    unsigned r = blockIdx.x * wpc + (unsigned)wid;
+    if (r >= n) return;
+    const unsigned last = n - 1;
+    const unsigned ldx_b = (unsigned)a.ldx * 4u;
+    const int steps = MODE == kEarly ? a.max_iter : min(a.hard_cap, RTK_FAST_STEPS);
+    if constexpr (MASKED) {  // padding chunks: NaN once (load_smem_prefilled)
+        Row::fill_slot_nan(ringA, lane, kSlot);
+        Row::fill_slot_nan(ringB, lane, kSlot);
+        __syncwarp();
+    }
+    Row::stage_async(row_ptr(a.x, r, ldx_b), a.m, lane, ringA, 0u);
+    Row::stage_async(row_ptr(a.x, min(r + nw, last), ldx_b), a.m, lane, ringB, 0u);
+    cp_async_commit();
+    Row A, B;
+    for (;;) {
+        cp_async_wait<0>();  // this lane's copies have landed ...
+        __syncwarp();        // ... and every lane's (chunks go to their owner lanes)
+        A.load_smem_prefilled(ringA, lane);
+        B.load_smem_prefilled(ringB, lane);
+        const unsigned rn = r + 2u * nw;
+        process_pair<MODE, false, float>(A, B, r, r + nw, r + nw < n, a, lane, sA, sB, steps, [&](unsigned tok) {
+            __syncwarp();  // every lane has read both slots before any refill lands
+            const unsigned salt = tok & a.opaque_zero;
+            if (rn < n) {
+                Row::stage_async(row_ptr(a.x, rn + salt, ldx_b), a.m, lane, ringA, salt);
+                Row::stage_async(row_ptr(a.x, min(rn + nw, last) + salt, ldx_b), a.m, lane, ringB, salt);
+            }
+            cp_async_commit();
+        });
+        if (rn >= n) break;
+        r = rn;
+    }
+    cp_async_wait<0>();
+}
+
 }  // namespace rtk
 
 // ---------------------------------------------------------------------------

@@ -156,6 +156,26 @@ int launch_big_pair_tma_kernel(const rtk::Args& a, cudaStream_t s, const CUtenso
     return RTK_OK;
 }
 
+// Paired long rows through the cp.async ring (rtk_big.cuh): E <= 32 rows the
+// TMA path does not take (E = 12..28, masked rows).
+#ifndef RTK_BIG_PAIR_CP
+#define RTK_BIG_PAIR_CP 1
+#endif
+template <int MODE, int E, bool MASKED>
+int launch_big_pair_kernel(const rtk::Args& a, cudaStream_t s) {
+    using Row = rtk::LaneRowCut<E, MASKED>;
+    const size_t per_warp = 2 * (Row::stage_bytes(a.k) + Row::kRowBytes);
+    constexpr int wpc = RTK_BIG_THREADS / 32;
+    return launch_rows(rtk::rowtopk_big_pair_kernel<MODE, E, MASKED>, a, s, (size_t)wpc * per_warp, RTK_BIG_THREADS, 2);
+}
+
+template <int MODE>
+bool big_pair_eligible(const rtk::Args& a) {
+    // early stop with k >= 128 measured 6% slower paired (two k-pair flushes per step)
+    return MODE != rtk::kTrace && a.iters == nullptr && a.reasons == nullptr && a.n < (1LL << 30) &&
+           (MODE == rtk::kEarly ? a.k < 128 : a.eps_rel == 0.0);
+}
+
 template <int MODE, int E, bool MASKED>
 int launch_big(const rtk::Args& a, cudaStream_t s) {
     if constexpr (RTK_USE_TMA && !MASKED && (E == 16 || E == 32)) {
@@ -165,10 +185,7 @@ int launch_big(const rtk::Args& a, cudaStream_t s) {
 #define RTK_BIG_PAIR_E32 1
 #endif
             if constexpr (RTK_BIG_PAIR && (E == 16 || (RTK_BIG_PAIR_E32 && E == 32)) && MODE != rtk::kTrace) {
-                // early stop with k >= 128 measured 6% slower paired (two k-pair flushes per step)
-                if (a.iters == nullptr && a.reasons == nullptr && a.n < (1LL << 30) &&
-                    (MODE == rtk::kEarly ? a.k < 128 : a.eps_rel == 0.0))
-                    return launch_big_pair_tma_kernel<MODE, E>(a, s, map);
+                if (big_pair_eligible<MODE>(a)) return launch_big_pair_tma_kernel<MODE, E>(a, s, map);
             }
             if constexpr (MODE == rtk::kTrace) {
                 return launch_big_tma_kernel<MODE, E, true>(a, s, map);
@@ -179,6 +196,9 @@ int launch_big(const rtk::Args& a, cudaStream_t s) {
                 return launch_big_tma_kernel<MODE, E, false>(a, s, map);
             }
         }
+    }
+    if constexpr (RTK_BIG_PAIR_CP && E <= 32 && MODE != rtk::kTrace) {
+        if (big_pair_eligible<MODE>(a)) return launch_big_pair_kernel<MODE, E, MASKED>(a, s);
     }
     if constexpr (MODE == rtk::kTrace) {
         return launch_big_kernel<MODE, E, MASKED, true>(a, s);
