@@ -111,15 +111,17 @@ __global__ void __launch_bounds__(BigThreads<E>::value, BigMinCtas<E, MASKED>::v
 // Paired long rows through the cp.async ring (E = 12..32 incl. masked rows,
 // where the TMA map does not apply): two ring slots per warp, refilled with
 // the next pair once both tiles are in registers; same pair scheme as above.
-template <int E>
-struct BigPairCpMinCtas {
-    static constexpr int value = E <= 16 ? 4 : 2;
+template <int E, class In>
+struct BigPairCpMinCtas {  // 16-bit rows need the widening registers too: 128 registers
+    static constexpr int value = (E <= 16 && std::is_same<In, float>::value) ? 4 : 2;
 };
 
-template <int MODE, int E, bool MASKED>
-__global__ void __launch_bounds__(RTK_BIG_THREADS, BigPairCpMinCtas<E>::value) rowtopk_big_pair_kernel(Args a) {
+template <int MODE, int E, bool MASKED, class In = float>
+__global__ void __launch_bounds__(RTK_BIG_THREADS, BigPairCpMinCtas<E, In>::value) rowtopk_big_pair_kernel(Args a) {
     using Row = LaneRowCut<E, MASKED>;
-    constexpr unsigned kSlot = Row::kRowBytes;
+    constexpr bool kF32 = std::is_same<In, float>::value;
+    constexpr unsigned kSlot = kF32 ? Row::kRowBytes : Row::kRowBytes16;
+    const In* __restrict__ x = reinterpret_cast<const In*>(a.x);
     extern __shared__ __align__(16) float smem[];
     const int lane = threadIdx.x & 31;
     const int wid = __shfl_sync(kFull, (int)(threadIdx.x >> 5), 0);
@@ -135,29 +137,41 @@ __global__ void __launch_bounds__(RTK_BIG_THREADS, BigPairCpMinCtas<E>::value) r
     unsigned r = blockIdx.x * wpc + (unsigned)wid;
     if (r >= n) return;
     const unsigned last = n - 1;
-    const unsigned ldx_b = (unsigned)a.ldx * 4u;
+    const unsigned ldx_b = (unsigned)a.ldx * (unsigned)sizeof(In);
     const int steps = MODE == kEarly ? a.max_iter : min(a.hard_cap, RTK_FAST_STEPS);
-    if constexpr (MASKED) {  // padding chunks: NaN once (load_smem_prefilled)
+    if constexpr (MASKED) {  // padding chunks: NaN once (load_smem_prefilled / NaN halves)
         Row::fill_slot_nan(ringA, lane, kSlot);
         Row::fill_slot_nan(ringB, lane, kSlot);
         __syncwarp();
     }
-    Row::stage_async(row_ptr(a.x, r, ldx_b), a.m, lane, ringA, 0u);
-    Row::stage_async(row_ptr(a.x, min(r + nw, last), ldx_b), a.m, lane, ringB, 0u);
+    auto stage = [&](unsigned row, unsigned slot, unsigned salt) {
+        if constexpr (kF32)
+            Row::stage_async(row_ptr(x, row, ldx_b), a.m, lane, slot, salt);
+        else
+            Row::template stage_async16<In>(row_ptr(x, row, ldx_b), a.m, lane, slot, salt);
+    };
+    auto load = [&](Row& R, unsigned slot) {
+        if constexpr (kF32)
+            R.load_smem_prefilled(slot, lane);
+        else
+            R.template load_smem16<In>(slot, lane);
+    };
+    stage(r, ringA, 0u);
+    stage(min(r + nw, last), ringB, 0u);
     cp_async_commit();
     Row A, B;
     for (;;) {
         cp_async_wait<0>();  // this lane's copies have landed ...
         __syncwarp();        // ... and every lane's (chunks go to their owner lanes)
-        A.load_smem_prefilled(ringA, lane);
-        B.load_smem_prefilled(ringB, lane);
+        load(A, ringA);
+        load(B, ringB);
         const unsigned rn = r + 2u * nw;
-        process_pair<MODE, false, float>(A, B, r, r + nw, r + nw < n, a, lane, sA, sB, steps, [&](unsigned tok) {
+        process_pair<MODE, false, In>(A, B, r, r + nw, r + nw < n, a, lane, sA, sB, steps, [&](unsigned tok) {
             __syncwarp();  // every lane has read both slots before any refill lands
             const unsigned salt = tok & a.opaque_zero;
             if (rn < n) {
-                Row::stage_async(row_ptr(a.x, rn + salt, ldx_b), a.m, lane, ringA, salt);
-                Row::stage_async(row_ptr(a.x, min(rn + nw, last) + salt, ldx_b), a.m, lane, ringB, salt);
+                stage(rn + salt, ringA, salt);
+                stage(min(rn + nw, last) + salt, ringB, salt);
             }
             cp_async_commit();
         });

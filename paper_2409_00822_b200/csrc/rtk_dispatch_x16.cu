@@ -30,8 +30,26 @@ int launch_big16_kernel(const rtk::Args& a, cudaStream_t s) {
     return launch_rows(rtk::rowtopk_big_kernel<MODE, E, MASKED, false, In>, a, s, (size_t)wpc * per_warp, 32 * wpc);
 }
 
+// Paired long rows (rtk_big.cuh, as rtk_dispatch.cuh's launch_big_pair_kernel)
+template <int MODE, int E, bool MASKED, class In>
+int launch_big16_pair_kernel(const rtk::Args& a, cudaStream_t s) {
+    using namespace rtk_dispatch;
+    using Row = rtk::LaneRowCut<E, MASKED>;
+    const size_t per_warp = 2 * (Row::stage_bytes(a.k) + Row::kRowBytes16);
+    constexpr int wpc = RTK_BIG_THREADS / 32;
+    return launch_rows(rtk::rowtopk_big_pair_kernel<MODE, E, MASKED, In>, a, s, (size_t)wpc * per_warp,
+                       RTK_BIG_THREADS, 2);
+}
+
 template <int MODE, int E, class In>
 int launch_big16(const rtk::Args& a, cudaStream_t s) {
+    // (paired 16-bit tiles spill above E = 20 even at 128 registers: E <= 20 only)
+    if constexpr (RTK_BIG_PAIR_CP && E <= 20) {
+        if (rtk_dispatch::big_pair_eligible<MODE>(a)) {
+            if (a.m == 32 * E) return launch_big16_pair_kernel<MODE, E, false, In>(a, s);
+            return launch_big16_pair_kernel<MODE, E, true, In>(a, s);
+        }
+    }
     if (a.m == 32 * E) return launch_big16_kernel<MODE, E, false, In>(a, s);
     return launch_big16_kernel<MODE, E, true, In>(a, s);
 }
