@@ -12,10 +12,13 @@
 // tiles once the current pair has been read (see rowtopk_kernel).
 //
 // Used for launches without traces on the lane-contiguous register tile
-// (M <= 1024, M % 4 == 0, 16-byte aligned rows) in early-stop mode and in
-// exact mode with eps_rel == 0.  Rows that cannot take the fast loop
-// (degenerate, |min| or |max| >= 2^126, NaN) and unpaired last rows run the
-// general per-row path (row_body).  Outputs are those of rowtopk_kernel.
+// (M <= 256 here, M % 4 == 0, 16-byte aligned rows; the paired long-row
+// kernels of rtk_big.cuh reuse process_pair for 256 < M <= 1024) in
+// early-stop mode and in exact mode with eps_rel == 0.  Rows that cannot take
+// the fast loop (degenerate, |min| or |max| >= 2^126, NaN) and unpaired last
+// rows run the general per-row path (row_body).  Outputs are those of
+// rowtopk_kernel.  Both rows' midpoints are one FADD2 + FMUL2 and both rows'
+// compare sums one f32x2 tree (mid_fast2, lane_count_ge2).
 #pragma once
 
 #include "rtk_kernels.cuh"
@@ -198,8 +201,9 @@ __device__ __forceinline__ void finish_exact(const Row& row, const Args& a, int 
 // sbase + kIdxOff by every path: select_flush_pair, finish_exact, row_body),
 // write the dense MaxK row -- x with all but the selected entries set to
 // +0 -- and / or a uint8 copy of the indices (the compact index layout of
-// the MaxK sparse rows for M <= 256), straight from the register tile: the staged indices set bits of a
-// 32E-bit shared bitmap (atomic OR), then each lane stores its E contiguous
+// the MaxK sparse rows for M <= 256), straight from the register tile: the
+// staged indices set bits of a 32E-bit shared bitmap (atomic OR), then each
+// lane stores its E contiguous
 // elements (value or zero) with vector stores in the input type (16-bit
 // rows: the tile holds their exact fp32 widening, narrowed back exactly).
 // Replaces the select -> scatter_rows pair (one launch and the N*k*8-byte
