@@ -540,3 +540,31 @@ def test_output_row_strides_and_alignment(oracle_lib):
                 assert np.array_equal(i[:, :k], want[1]), ctx
                 assert np.array_equal(_bits(v[:, :k]), _bits(want[0])), ctx
                 assert (v[:, k:] == 7.0).all() and (i[:, k:] == -1).all(), ctx
+
+
+@pytest.mark.parametrize("m", [384, 500, 512, 640, 1000, 1024])
+def test_paired_long_rows_adversarial(oracle_lib, m):
+    """The paired long-row kernels (TMA slots at M = 512 / 1024, the cp.async
+    ring otherwise, masked rows at 500 / 1000) on rows that leave the fast
+    loop: tie-heavy and constant rows, ±inf and huge rows (general path in the
+    pair), tiny hard caps (finish_exact after the pair loop), odd N (unpaired
+    last row), a strided view; exact and early stop (k < 128 paired, k >= 128
+    single-row), bit-exact against the oracle."""
+    rng = np.random.default_rng(m)
+    n = 777
+    base = rng.standard_normal((n, m + 12)).astype(np.float32)
+    base[1::7] = rng.integers(-2, 3, (len(range(1, n, 7)), m + 12)).astype(np.float32)  # ties at the k-th value
+    base[3] = 0.5                                                                      # constant row
+    base[10, 5] = np.inf
+    base[11, 7] = -np.inf
+    base[12, :3] = 3e38                                                                # |max| >= 2^126
+    x_host = np.ascontiguousarray(base[:, 4:4 + m])
+    xd = torch.from_numpy(base).cuda()[:, 4:4 + m]                                     # strided device view
+    for k in (1, 33, 127, 128, m - 1):
+        for mode, mi, cap in (("exact", 4, 64), ("exact", 4, 5), ("early", 3, 64), ("early", 9, 64)):
+            search = (rtk.SearchConfig.exact(hard_cap=cap) if mode == "exact"
+                      else rtk.SearchConfig.early_stop(mi))
+            v, i, _, _ = oracle_lib.ref_batch(x_host, k, mode, max_iter=mi, hard_cap=cap)
+            res = rtk.batch_topk(xd, rtk.BatchConfig(k=k, search=search))
+            assert np.array_equal(res.indices.cpu().numpy(), i), (m, k, mode, mi, cap)
+            assert np.array_equal(res.values.cpu().numpy().view(np.uint32), v.view(np.uint32)), (m, k, mode, mi, cap)
