@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(RTK_BIG_THREADS, BigPairCpMinCtas<E, In>::valu
     const int wid = __shfl_sync(kFull, (int)(threadIdx.x >> 5), 0);
     const unsigned wpc = blockDim.x >> 5;
     const unsigned base = (unsigned)__cvta_generic_to_shared(smem);
-    const unsigned stage_bytes = Row::stage_bytes(a.k);
+    const unsigned stage_bytes = pair_stage_bytes<Row>(a.k);  // k-pair staging or the candidate set
     const unsigned sA = base + (unsigned)wid * 2u * stage_bytes;
     const unsigned sB = sA + stage_bytes;
     const unsigned ringA = base + wpc * 2u * stage_bytes + (unsigned)wid * 2u * kSlot;
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(RTK_BIG_THREADS, BigPairMinCtas<E>::value) row
     const int wid = __shfl_sync(kFull, (int)(threadIdx.x >> 5), 0);
     const unsigned wpc = blockDim.x >> 5;
     const unsigned base = (unsigned)__cvta_generic_to_shared(smem);
-    const unsigned stage_bytes = Row::stage_bytes(a.k);
+    const unsigned stage_bytes = pair_stage_bytes<Row>(a.k);  // k-pair staging or the candidate set
     const unsigned sA = base + (unsigned)wid * 2u * stage_bytes;
     const unsigned sB = sA + stage_bytes;
     const unsigned slots = (base + wpc * 2u * stage_bytes + Row::kSlotAlign - 1) & ~(Row::kSlotAlign - 1);

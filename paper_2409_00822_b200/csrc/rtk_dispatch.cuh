@@ -142,7 +142,7 @@ int launch_big_pair_tma_kernel(const rtk::Args& a, cudaStream_t s, const CUtenso
     using Row = rtk::TmaRow<E>;
     constexpr int wpc = RTK_BIG_THREADS / 32;
     const size_t smem =
-        (size_t)wpc * 2 * Row::stage_bytes(a.k) + Row::kSlotAlign + (size_t)wpc * (2 * Row::kSlotBytes + 8);
+        (size_t)wpc * 2 * rtk::pair_stage_bytes<Row>(a.k) + Row::kSlotAlign + (size_t)wpc * (2 * Row::kSlotBytes + 8);
     auto kernel = rtk::rowtopk_big_pair_tma_kernel<MODE, E>;
     if (describe(reinterpret_cast<const void*>(kernel), smem, RTK_BIG_THREADS, 2)) return RTK_OK;
     const long long blocks_needed = (a.n + 2 * wpc - 1) / (2 * wpc);
@@ -164,7 +164,7 @@ int launch_big_pair_tma_kernel(const rtk::Args& a, cudaStream_t s, const CUtenso
 template <int MODE, int E, bool MASKED>
 int launch_big_pair_kernel(const rtk::Args& a, cudaStream_t s) {
     using Row = rtk::LaneRowCut<E, MASKED>;
-    const size_t per_warp = 2 * (Row::stage_bytes(a.k) + Row::kRowBytes);
+    const size_t per_warp = 2 * (rtk::pair_stage_bytes<Row>(a.k) + Row::kRowBytes);
     constexpr int wpc = RTK_BIG_THREADS / 32;
     return launch_rows(rtk::rowtopk_big_pair_kernel<MODE, E, MASKED>, a, s, (size_t)wpc * per_warp, RTK_BIG_THREADS, 2);
 }

@@ -35,7 +35,7 @@ template <int MODE, int E, bool MASKED, class In>
 int launch_big16_pair_kernel(const rtk::Args& a, cudaStream_t s) {
     using namespace rtk_dispatch;
     using Row = rtk::LaneRowCut<E, MASKED>;
-    const size_t per_warp = 2 * (Row::stage_bytes(a.k) + Row::kRowBytes16);
+    const size_t per_warp = 2 * (rtk::pair_stage_bytes<Row>(a.k) + Row::kRowBytes16);
     constexpr int wpc = RTK_BIG_THREADS / 32;
     return launch_rows(rtk::rowtopk_big_pair_kernel<MODE, E, MASKED, In>, a, s, (size_t)wpc * per_warp,
                        RTK_BIG_THREADS, 2);

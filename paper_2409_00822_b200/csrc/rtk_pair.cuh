@@ -270,6 +270,242 @@ __device__ __forceinline__ void dense_row(const Row& R, unsigned sbase, const Ar
     __syncwarp();  // the bitmap and the staging are reused by the next row
 }
 
+// Row r of the input into a register tile: fp32 rows as they are, 16-bit
+// rows (In = __nv_bfloat16 / __half, rtk_rowtopk_x16) widened on load.
+template <class In, class Row>
+__device__ __forceinline__ void load_tile(Row& R, const Args& a, unsigned r, unsigned ldx_b, int lane) {
+    if constexpr (std::is_same<In, float>::value)
+        R.load(row_ptr(a.x, r, ldx_b), a.m, lane);
+    else
+        R.template load16<In>(row_ptr(reinterpret_cast<const In*>(a.x), r, ldx_b), a.m, lane);
+}
+
+// ------------------------------------ exact mode, long rows: candidate set
+//
+// For the paired long-row kernels (LaneRowCut tiles, E = 12..32) the exact
+// search runs in two phases.  Full phase: reference bisection steps counting
+// the whole tile, until the count at the bracket's lower end mn is at most
+// the candidate capacity 32 C (or cnt == k).  Every later midpoint is >= mn,
+// so counting the candidate set S = {v >= mn} gives the reference's count;
+// S is staged as (value, index) pairs in index order (one packed warp scan
+// for both rows) and read back C slots per lane.  Candidate phase: the same
+// reference steps (same midpoints, same decisions) on S -- C compares per
+// lane instead of E.  Selection: S at the final midpoint (cnt == k) by one
+// ballot prefix per slot, written straight to the output row.  A row meeting
+// cnt == k in the full phase stages S = {v >= mid} (k entries) and takes the
+// same selection; rows out of fast steps (stuck / tied) finish on the general
+// path (the tile is re-read).  At E = 8 (M = 256) the staging costs more than
+// the cheaper steps save (measured); at E >= 12 a full step costs 1.5 E + 13
+// instructions per row and a candidate step about 15.
+#ifndef RTK_LONG_CAND
+#define RTK_LONG_CAND 1
+#endif
+constexpr int kLongCandMaxSlots = 4;
+// staging bytes per row of the paired long-row kernels: the k-pair staging
+// of LaneRowCut or the candidate set, whichever is larger
+template <class Row>
+__host__ __device__ constexpr unsigned pair_stage_bytes(int k) {
+    return Row::stage_bytes(k) > 8u * 32u * kLongCandMaxSlots ? Row::stage_bytes(k) : 8u * 32u * kLongCandMaxSlots;
+}
+
+template <int C>
+struct CandSet {
+    float v[C];
+    int i[C];
+};
+
+// Stage this lane's elements with v >= t as (value, index) pairs at entries
+// excl, excl + 1, ... of the list at sbase.
+template <class Row>
+__device__ __forceinline__ void stage_cand(const Row& R, float t, unsigned sbase, int lane, unsigned excl) {
+    constexpr int E = Row::kSlots;
+    unsigned addr = sbase + 8u * excl;
+    const int i0 = lane * E;
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+        if (R.v[q] >= t) {
+            asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(__float_as_int(R.v[q])), "r"(i0 + q)
+                         : "memory");
+            addr += 8u;
+        }
+    }
+}
+
+// Entries j = lane + 32 q of the staged list (ns of them); past ns: NaN.
+template <int C>
+__device__ __forceinline__ void load_cand(unsigned sbase, int lane, int ns, CandSet<C>& S) {
+#pragma unroll
+    for (int q = 0; q < C; ++q) {
+        const int j = lane + 32 * q;
+        int x, i;
+        asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(x), "=r"(i) : "r"(sbase + 8u * j) : "memory");
+        S.i[q] = i;
+        S.v[q] = j < ns ? __int_as_float(x) : __int_as_float(0x7fffffff);
+    }
+}
+
+// Biased lane counts of both rows' candidates >= tA / tB (one FADD2 per slot).
+template <int C>
+__device__ __forceinline__ void cand_count2(const CandSet<C>& SA, const CandSet<C>& SB, float tA, float tB, int& lA,
+                                            int& lB) {
+    float xa = 0x1p23f, xb = 0x1p23f;
+#pragma unroll
+    for (int q = 0; q < C; ++q) add2(xa, xb, set_ge(SA.v[q], tA), set_ge(SB.v[q], tB));
+    lA = __float_as_int(xa);
+    lB = __float_as_int(xb);
+}
+
+template <int C>
+__device__ __forceinline__ void cand_steps_alone(const CandSet<C>& S, int kb, int steps, float& mn, float& mx,
+                                                 float& mid, int& c, int& it) {
+#pragma unroll 1
+    while (c != kb && it < steps) {
+        ++it;
+        mid = mid_fast(mn, mx);
+        float x = 0x1p23f;
+#pragma unroll
+        for (int q = 0; q < C; ++q) x = __fadd_rn(x, set_ge(S.v[q], mid));
+        c = warp_count(__float_as_int(x));
+        const bool lt = c < kb;
+        mx = lt ? mid : mx;
+        mn = lt ? mn : mid;
+    }
+}
+
+// Full-phase steps of one row until cnt == k, the count at mn is <= the
+// capacity (clb, hl: biased row / lane counts at mn), or `steps`.
+template <class Row>
+__device__ __forceinline__ void full_steps_alone(const Row& R, int kb, int capb, int steps, float& mn, float& mx,
+                                                 float& mid, int& c, int& l, int& hl, int& clb, int& it) {
+#pragma unroll 1
+    while (c != kb && clb > capb && it < steps) {
+        ++it;
+        mid = mid_fast(mn, mx);
+        l = R.lane_count_ge(mid);
+        c = warp_count(l);
+        const bool lt = c < kb;
+        mx = lt ? mid : mx;
+        mn = lt ? mn : mid;
+        hl = lt ? hl : l;
+        clb = lt ? clb : c;
+    }
+}
+
+// The candidates >= t (exactly k of them) in index order, to the output row.
+template <int C>
+__device__ __forceinline__ void emit_cand(const CandSet<C>& S, float t, float* __restrict__ ov,
+                                          int* __restrict__ oi) {
+    const unsigned lt = lanemask_lt();
+    int base = 0;
+#pragma unroll
+    for (int q = 0; q < C; ++q) {
+        const bool p = S.v[q] >= t;
+        const unsigned b = __ballot_sync(kFull, p);
+        const int pos = base + __popc(b & lt);
+        if (p) {
+            ov[pos] = S.v[q];
+            oi[pos] = S.i[q];
+        }
+        base += __popc(b);
+    }
+}
+
+template <int C, class In, class Row>
+__device__ __forceinline__ void exact_pair_cand(const Row& A, const Row& B, unsigned rA, unsigned rB, const Args& a,
+                                                int lane, unsigned sA, unsigned sB, int steps, float mnA, float mxA,
+                                                float mnB, float mxB, float* __restrict__ ovA, int* __restrict__ oiA,
+                                                float* __restrict__ ovB, int* __restrict__ oiB) {
+    const int k = a.k;
+    const int kb = k + kCountBias;
+    const int capb = 32 * C + kCountBias;
+    float midA, midB;
+    int cA, cB, lA, lB, it = 0;
+    int hA = (int)kLaneBias + Row::lane_valid(a.m, lane), hB = hA;  // lane counts at mn
+    int clA = a.m + kCountBias, clB = clA;                          // row counts at mn
+#pragma unroll 1
+    do {
+        ++it;
+        mid_fast2(mnA, mxA, mnB, mxB, midA, midB);
+        lane_count_ge2(A, B, midA, midB, lA, lB);
+        cA = warp_count(lA);
+        cB = warp_count(lB);
+        const bool ltA = cA < kb, ltB = cB < kb;
+        mxA = ltA ? midA : mxA;
+        mnA = ltA ? mnA : midA;
+        hA = ltA ? hA : lA;
+        clA = ltA ? clA : cA;
+        mxB = ltB ? midB : mxB;
+        mnB = ltB ? mnB : midB;
+        hB = ltB ? hB : lB;
+        clB = ltB ? clB : cB;
+    } while (cA != kb && cB != kb && clA > capb && clB > capb && it < steps);
+    int itA = it, itB = it;
+    full_steps_alone(A, kb, capb, steps, mnA, mxA, midA, cA, lA, hA, clA, itA);
+    full_steps_alone(B, kb, capb, steps, mnB, mxB, midB, cB, lB, hB, clB, itB);
+    bool eqA = cA == kb, eqB = cB == kb;
+    if (!((eqA || clA <= capb) && (eqB || clB <= capb))) {  // out of fast steps (cold)
+        finish_exact(A, a, lane, sA, eqA, mnA, mxA, midA, cA, itA, lA, ovA, oiA);
+        finish_exact(B, a, lane, sB, eqB, mnB, mxB, midB, cB, itB, lB, ovB, oiB);
+        return;
+    }
+    // S = {v >= T} of both rows (T = mid on cnt == k, else mn)
+    const float tA = eqA ? midA : mnA, tB = eqB ? midB : mnB;
+    const int nA = eqA ? k : clA - kCountBias, nB = eqB ? k : clB - kCountBias;
+    const unsigned HA = (unsigned)((eqA ? lA : hA) - (int)kLaneBias), HB = (unsigned)((eqB ? lB : hB) - (int)kLaneBias);
+    const unsigned packed = HA | (HB << 16);
+    const unsigned excl = warp_incl_scan_nv(packed) - packed;
+    stage_cand(A, tA, sA, lane, excl & 0xffffu);
+    stage_cand(B, tB, sB, lane, excl >> 16);
+    __syncwarp();
+    CandSet<C> SA, SB;
+    load_cand(sA, lane, nA, SA);
+    load_cand(sB, lane, nB, SB);
+    __syncwarp();
+    if (!eqA && !eqB && itA < steps && itB < steps) {  // (the full phase may have used up the steps)
+#pragma unroll 1
+        do {
+            ++itA;
+            ++itB;
+            mid_fast2(mnA, mxA, mnB, mxB, midA, midB);
+            int lcA, lcB;
+            cand_count2(SA, SB, midA, midB, lcA, lcB);
+            cA = warp_count(lcA);
+            cB = warp_count(lcB);
+            const bool ltA = cA < kb, ltB = cB < kb;
+            mxA = ltA ? midA : mxA;
+            mnA = ltA ? mnA : midA;
+            mxB = ltB ? midB : mxB;
+            mnB = ltB ? mnB : midB;
+        } while (cA != kb && cB != kb && itA < steps && itB < steps);  // the rows' counts differ after the full phase
+    }
+    cand_steps_alone(SA, kb, steps, mnA, mxA, midA, cA, itA);
+    cand_steps_alone(SB, kb, steps, mnB, mxB, midB, cB, itB);
+    eqA = cA == kb;
+    eqB = cB == kb;
+    if (eqA && eqB) {
+        emit_cand(SA, midA, ovA, oiA);
+        emit_cand(SB, midB, ovB, oiB);
+        return;
+    }
+    // out of fast steps in the candidate phase (cold): the general path on a
+    // re-read tile
+    const unsigned ldx_b = (unsigned)a.ldx * (unsigned)sizeof(In);
+    if (eqA) {
+        emit_cand(SA, midA, ovA, oiA);
+    } else {
+        Row T;
+        load_tile<In>(T, a, rA, ldx_b, lane);
+        finish_exact(T, a, lane, sA, false, mnA, mxA, midA, cA, itA, T.lane_count_ge(midA), ovA, oiA);
+    }
+    if (eqB) {
+        emit_cand(SB, midB, ovB, oiB);
+    } else {
+        Row T;
+        load_tile<In>(T, a, rB, ldx_b, lane);
+        finish_exact(T, a, lane, sB, false, mnB, mxB, midB, cB, itB, T.lane_count_ge(midB), ovB, oiB);
+    }
+}
+
 // mn0 < mx0 with both inside (-2^126, 2^126): non-degenerate (both modes),
 // finite (exact mode's eps_rel == 0 loop test) and overflow-free midpoints.
 // NaN compares false.
@@ -279,7 +515,7 @@ __device__ __forceinline__ bool fast_eligible(float mn0, float mx0) {
 
 // One pair of rows (rA = r, rB = r + nw when hasB).  `after_load(token)`
 // issues the next pair's loads once both tiles have been read.
-template <int MODE, class Row, class Hook>
+template <int MODE, class In, class Row, class Hook>
 __device__ __forceinline__ void process_pair_sel(const Row& A, const Row& B, unsigned rA, unsigned rB, bool hasB,
                                                  const Args& a, int lane, unsigned sA, unsigned sB, int steps,
                                                  const Hook& after_load) {
@@ -327,6 +563,16 @@ __device__ __forceinline__ void process_pair_sel(const Row& A, const Row& B, uns
         // (scalar flush: the vectorised one measured 2% slower in early-stop mode)
         select_two(A, B, mnA, mnB, hA, hB, sA, sB, lane, k, ovA, oiA, ovB, oiB, false, a.opaque_zero);
     } else {
+        if constexpr (RTK_LONG_CAND && Row::kPad == 0) {  // long rows: the candidate-set search above
+            if (k <= 40) {
+                exact_pair_cand<2, In>(A, B, rA, rB, a, lane, sA, sB, steps, mnA, mxA, mnB, mxB, ovA, oiA, ovB, oiB);
+                return;
+            }
+            if (k <= 96) {
+                exact_pair_cand<4, In>(A, B, rA, rB, a, lane, sA, sB, steps, mnA, mxA, mnB, mxB, ovA, oiA, ovB, oiB);
+                return;
+            }
+        }
         // Algorithm 1 fast steps (exact_loop_fast) on both rows until either
         // meets cnt == k; the other continues alone.
         float midA, midB;
@@ -364,21 +610,11 @@ template <int MODE, bool DENSE, class In, class Row, class Hook>
 __device__ __forceinline__ void process_pair(const Row& A, const Row& B, unsigned rA, unsigned rB, bool hasB,
                                              const Args& a, int lane, unsigned sA, unsigned sB, int steps,
                                              const Hook& after_load) {
-    process_pair_sel<MODE>(A, B, rA, rB, hasB, a, lane, sA, sB, steps, after_load);
+    process_pair_sel<MODE, In>(A, B, rA, rB, hasB, a, lane, sA, sB, steps, after_load);
     if constexpr (DENSE) {
         dense_row<In>(A, sA, a, rA, lane);
         if (hasB) dense_row<In>(B, sB, a, rB, lane);
     }
-}
-
-// Row r of the input into a register tile: fp32 rows as they are, 16-bit
-// rows (In = __nv_bfloat16 / __half, rtk_rowtopk_x16) widened on load.
-template <class In, class Row>
-__device__ __forceinline__ void load_tile(Row& R, const Args& a, unsigned r, unsigned ldx_b, int lane) {
-    if constexpr (std::is_same<In, float>::value)
-        R.load(row_ptr(a.x, r, ldx_b), a.m, lane);
-    else
-        R.template load16<In>(row_ptr(reinterpret_cast<const In*>(a.x), r, ldx_b), a.m, lane);
 }
 
 // Persistent loop over row pairs (r, r + nw), stepping 2 nw; register
