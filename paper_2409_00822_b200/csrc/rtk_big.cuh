@@ -116,7 +116,7 @@ struct BigPairCpMinCtas {  // 16-bit rows need the widening registers too: 128 r
     static constexpr int value = (E <= 16 && std::is_same<In, float>::value) ? 4 : 2;
 };
 
-template <int MODE, int E, bool MASKED, class In = float>
+template <int MODE, int E, bool MASKED, class In = float, int CMAX = 4>
 __global__ void __launch_bounds__(RTK_BIG_THREADS, BigPairCpMinCtas<E, In>::value) rowtopk_big_pair_kernel(Args a) {
     using Row = LaneRowCut<E, MASKED>;
     constexpr bool kF32 = std::is_same<In, float>::value;
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(RTK_BIG_THREADS, BigPairCpMinCtas<E, In>::valu
         load(A, ringA);
         load(B, ringB);
         const unsigned rn = r + 2u * nw;
-        process_pair<MODE, false, In>(A, B, r, r + nw, r + nw < n, a, lane, sA, sB, steps, [&](unsigned tok) {
+        process_pair<MODE, false, In, CMAX>(A, B, r, r + nw, r + nw < n, a, lane, sA, sB, steps, [&](unsigned tok) {
             __syncwarp();  // every lane has read both slots before any refill lands
             const unsigned salt = tok & a.opaque_zero;
             if (rn < n) {
@@ -308,7 +308,7 @@ struct BigPairMinCtas {  // E = 16: 64 registers (4 CTAs of 8 warps); E = 32: tw
     static constexpr int value = E <= 16 ? 4 : 2;
 };
 
-template <int MODE, int E>
+template <int MODE, int E, int CMAX = 4>
 __global__ void __launch_bounds__(RTK_BIG_THREADS, BigPairMinCtas<E>::value) rowtopk_big_pair_tma_kernel(Args a,
                                                                                 const __grid_constant__ CUtensorMap map) {
     using Row = TmaRow<E>;
@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(RTK_BIG_THREADS, BigPairMinCtas<E>::value) row
         A.load_swizzled(slotA, lane);
         B.load_swizzled(slotB, lane);
         const unsigned rn = r + 2u * nw;
-        process_pair<MODE, false, float>(A, B, r, r + nw, r + nw < n, a, lane, sA, sB, steps, [&](unsigned tok) {
+        process_pair<MODE, false, float, CMAX>(A, B, r, r + nw, r + nw < n, a, lane, sA, sB, steps, [&](unsigned tok) {
             __syncwarp();  // every lane has read both slots
             if (lane == 0 && rn < n) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -137,13 +137,16 @@ int launch_big_tma_kernel(const rtk::Args& a, cudaStream_t s, const CUtensorMap&
 
 // Paired long rows on TMA slots (rtk_big.cuh): E = 16, no traces, exact
 // with eps_rel = 0 or early stop.
-template <int MODE, int E>
+template <int MODE, int E, int CMAX = 4>
 int launch_big_pair_tma_kernel(const rtk::Args& a, cudaStream_t s, const CUtensorMap& map) {
+    if constexpr (CMAX == 4 && MODE == rtk::kExact && E >= 24) {  // the 8-slot candidate search, own kernel
+        if (rtk::long_cand8<E>(a.k)) return launch_big_pair_tma_kernel<MODE, E, 8>(a, s, map);
+    }
     using Row = rtk::TmaRow<E>;
     constexpr int wpc = RTK_BIG_THREADS / 32;
     const size_t smem =
         (size_t)wpc * 2 * rtk::pair_stage_bytes<Row>(a.k) + Row::kSlotAlign + (size_t)wpc * (2 * Row::kSlotBytes + 8);
-    auto kernel = rtk::rowtopk_big_pair_tma_kernel<MODE, E>;
+    auto kernel = rtk::rowtopk_big_pair_tma_kernel<MODE, E, CMAX>;
     if (describe(reinterpret_cast<const void*>(kernel), smem, RTK_BIG_THREADS, 2)) return RTK_OK;
     const long long blocks_needed = (a.n + 2 * wpc - 1) / (2 * wpc);
     long long grid = (long long)rtk_device_sms() * rtk_ctas_per_sm(reinterpret_cast<const void*>(kernel), smem,
@@ -161,12 +164,15 @@ int launch_big_pair_tma_kernel(const rtk::Args& a, cudaStream_t s, const CUtenso
 #ifndef RTK_BIG_PAIR_CP
 #define RTK_BIG_PAIR_CP 1
 #endif
-template <int MODE, int E, bool MASKED>
+template <int MODE, int E, bool MASKED, int CMAX = 4>
 int launch_big_pair_kernel(const rtk::Args& a, cudaStream_t s) {
+    if constexpr (CMAX == 4 && MODE == rtk::kExact && E >= 24) {  // the 8-slot candidate search
+        if (rtk::long_cand8<E>(a.k)) return launch_big_pair_kernel<MODE, E, MASKED, 8>(a, s);
+    }
     using Row = rtk::LaneRowCut<E, MASKED>;
     const size_t per_warp = 2 * (rtk::pair_stage_bytes<Row>(a.k) + Row::kRowBytes);
     constexpr int wpc = RTK_BIG_THREADS / 32;
-    return launch_rows(rtk::rowtopk_big_pair_kernel<MODE, E, MASKED>, a, s, (size_t)wpc * per_warp, RTK_BIG_THREADS, 2);
+    return launch_rows(rtk::rowtopk_big_pair_kernel<MODE, E, MASKED, float, CMAX>, a, s, (size_t)wpc * per_warp, RTK_BIG_THREADS, 2);
 }
 
 template <int MODE>

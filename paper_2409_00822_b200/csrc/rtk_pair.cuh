@@ -300,12 +300,21 @@ __device__ __forceinline__ void load_tile(Row& R, const Args& a, unsigned r, uns
 #ifndef RTK_LONG_CAND
 #define RTK_LONG_CAND 1
 #endif
-constexpr int kLongCandMaxSlots = 4;
+// candidate slots per lane: 2 (k <= 40), 4 (k <= 96), 8 (k <= 192; E >= 24
+// only, in a separate kernel instantiation (CMAX = 8): at E = 16 the staging
+// would cost occupancy and a candidate step would count half the tile, and
+// compiled into the k <= 96 kernels the third search raised their spills)
+template <int E>
+__host__ __device__ constexpr bool long_cand8(int k) {
+    return E >= 24 && k > 96 && k <= 192;
+}
 // staging bytes per row of the paired long-row kernels: the k-pair staging
 // of LaneRowCut or the candidate set, whichever is larger
 template <class Row>
 __host__ __device__ constexpr unsigned pair_stage_bytes(int k) {
-    return Row::stage_bytes(k) > 8u * 32u * kLongCandMaxSlots ? Row::stage_bytes(k) : 8u * 32u * kLongCandMaxSlots;
+    const int slots = k <= 40 ? 2 : (k <= 96 ? 4 : (long_cand8<Row::kSlots>(k) ? 8 : 0));
+    const unsigned cand = 8u * 32u * (unsigned)slots;
+    return Row::stage_bytes(k) > cand ? Row::stage_bytes(k) : cand;
 }
 
 template <int C>
@@ -515,7 +524,7 @@ __device__ __forceinline__ bool fast_eligible(float mn0, float mx0) {
 
 // One pair of rows (rA = r, rB = r + nw when hasB).  `after_load(token)`
 // issues the next pair's loads once both tiles have been read.
-template <int MODE, class In, class Row, class Hook>
+template <int MODE, class In, int CMAX, class Row, class Hook>
 __device__ __forceinline__ void process_pair_sel(const Row& A, const Row& B, unsigned rA, unsigned rB, bool hasB,
                                                  const Args& a, int lane, unsigned sA, unsigned sB, int steps,
                                                  const Hook& after_load) {
@@ -564,13 +573,20 @@ __device__ __forceinline__ void process_pair_sel(const Row& A, const Row& B, uns
         select_two(A, B, mnA, mnB, hA, hB, sA, sB, lane, k, ovA, oiA, ovB, oiB, false, a.opaque_zero);
     } else {
         if constexpr (RTK_LONG_CAND && Row::kPad == 0) {  // long rows: the candidate-set search above
-            if (k <= 40) {
-                exact_pair_cand<2, In>(A, B, rA, rB, a, lane, sA, sB, steps, mnA, mxA, mnB, mxB, ovA, oiA, ovB, oiB);
+            if constexpr (CMAX >= 8) {  // launched for long_cand8(k) only
+                exact_pair_cand<8, In>(A, B, rA, rB, a, lane, sA, sB, steps, mnA, mxA, mnB, mxB, ovA, oiA, ovB, oiB);
                 return;
-            }
-            if (k <= 96) {
-                exact_pair_cand<4, In>(A, B, rA, rB, a, lane, sA, sB, steps, mnA, mxA, mnB, mxB, ovA, oiA, ovB, oiB);
-                return;
+            } else {
+                if (k <= 40) {
+                    exact_pair_cand<2, In>(A, B, rA, rB, a, lane, sA, sB, steps, mnA, mxA, mnB, mxB, ovA, oiA, ovB,
+                                           oiB);
+                    return;
+                }
+                if (k <= 96) {
+                    exact_pair_cand<4, In>(A, B, rA, rB, a, lane, sA, sB, steps, mnA, mxA, mnB, mxB, ovA, oiA, ovB,
+                                           oiB);
+                    return;
+                }
             }
         }
         // Algorithm 1 fast steps (exact_loop_fast) on both rows until either
@@ -606,11 +622,11 @@ __device__ __forceinline__ void process_pair_sel(const Row& A, const Row& B, uns
 }
 
 // The pair's selection, then (DENSE, rtk_maxk_dense) both fused MaxK rows.
-template <int MODE, bool DENSE, class In, class Row, class Hook>
+template <int MODE, bool DENSE, class In, int CMAX = 4, class Row, class Hook>
 __device__ __forceinline__ void process_pair(const Row& A, const Row& B, unsigned rA, unsigned rB, bool hasB,
                                              const Args& a, int lane, unsigned sA, unsigned sB, int steps,
                                              const Hook& after_load) {
-    process_pair_sel<MODE, In>(A, B, rA, rB, hasB, a, lane, sA, sB, steps, after_load);
+    process_pair_sel<MODE, In, CMAX>(A, B, rA, rB, hasB, a, lane, sA, sB, steps, after_load);
     if constexpr (DENSE) {
         dense_row<In>(A, sA, a, rA, lane);
         if (hasB) dense_row<In>(B, sB, a, rB, lane);

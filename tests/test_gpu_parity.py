@@ -570,17 +570,18 @@ def test_paired_long_rows_adversarial(oracle_lib, m):
             assert np.array_equal(res.values.cpu().numpy().view(np.uint32), v.view(np.uint32)), (m, k, mode, mi, cap)
 
 
-@pytest.mark.parametrize("m", [512, 768, 1000])
+@pytest.mark.parametrize("m", [512, 768, 1000, 1024])
 def test_long_row_candidate_search_boundaries(oracle_lib, m):
     """The candidate-set exact search of the paired long-row kernels at its
-    boundaries: k around the 2-slot / 4-slot / off switches (40, 41, 96, 97),
+    boundaries: k around the 2-slot / 4-slot / 8-slot / off switches (40, 41,
+    96, 97, 192, 193; 8 slots on rows of 768+ columns, its own kernel),
     hard caps small enough to end the search in the full phase, at the switch
     to the candidate phase, or inside it (1..6), and normal rows whose
     candidate set is close to the capacity; bit-exact vs the oracle."""
     rng = np.random.default_rng(7 * m)
     x = rng.standard_normal((401, m)).astype(np.float32)
     x[::9] = np.round(x[::9] * 4) / 4  # coarse values: ties near the k-th value
-    for k in (1, 16, 40, 41, 64, 96, 97):
+    for k in (1, 16, 40, 41, 64, 96, 97, 128, 192, 193):
         for cap in (1, 2, 3, 4, 5, 6, 64):
             v, i, _, _ = oracle_lib.ref_batch(x, k, "exact", hard_cap=cap)
             res = rtk.batch_topk(torch.from_numpy(x).cuda(), rtk.BatchConfig(k=k, search=rtk.SearchConfig.exact(hard_cap=cap)))
