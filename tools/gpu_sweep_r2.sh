@@ -1,12 +1,11 @@
 #!/bin/bash
-# Clock-recorded sweep (BASELINE configs[2..4] through bench.py) + ncu captures
+# Clock-recorded sweep (BASELINE configs[2..3] through bench.py; C5 is a leg of the default bench line) + ncu captures
 # of the M=128 and M=768 kernels.   bash tools/gpu_sweep_r2.sh TAG
 TAG=${1:-sweep}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu,power.draw --format=csv > $OUT/nvsmi.csv 2>&1
 timeout 1200 python bench.py --sweep --steps 50 --warmup 5 > $OUT/sweep.jsonl 2> $OUT/sweep.err
-timeout 600 python bench.py --workload c5 --no-cpu --no-e2e --no-torch --steps 20 --warmup 3 > $OUT/c5.json 2> $OUT/c5.err
 if [ "${NCU:-1}" = "1" ]; then
 for SH in 1048576:128:32 1048576:768:64; do
   for MODE in exact early; do
