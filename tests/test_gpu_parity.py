@@ -587,3 +587,35 @@ def test_long_row_candidate_search_boundaries(oracle_lib, m):
             res = rtk.batch_topk(torch.from_numpy(x).cuda(), rtk.BatchConfig(k=k, search=rtk.SearchConfig.exact(hard_cap=cap)))
             assert np.array_equal(res.indices.cpu().numpy(), i), (m, k, cap)
             assert np.array_equal(res.values.cpu().numpy().view(np.uint32), v.view(np.uint32)), (m, k, cap)
+
+
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16", "float16"])
+def test_long_row_paths_fuzz(oracle_lib, dtype):
+    """Randomised long rows (257 <= M <= 1024) through every regime of the
+    paired long-row kernels -- candidate sets of 2 / 4 / 8 slots and the full
+    search above them, hard caps that stop in either phase, early stop, odd N
+    (an unpaired last row), masked (M % 32 != 0) and unmasked tiles, mixed
+    and tie-heavy rows -- for fp32 and native 16-bit input (compared on the
+    float32 image); bit-exact vs the oracle."""
+    tdt = getattr(torch, dtype)
+    rng = np.random.default_rng({"float32": 5, "bfloat16": 6, "float16": 7}[dtype])
+    regimes = [(1, 40), (41, 96), (97, 192), (193, 400)]
+    for trial in range(120):
+        m = int(rng.choice([int(rng.integers(257, 1025)), int(rng.choice([384, 512, 640, 768, 896, 1024]))]))
+        if dtype != "float32":
+            m -= m % 8  # the native 16-bit long-row path takes M % 8 == 0
+        n = int(rng.integers(1, 120)) * 2 + 1
+        x = _mixed_rows(rng, n, m) if trial % 3 else rng.standard_normal((n, m)).astype(np.float32)
+        xd = torch.from_numpy(x).cuda().to(tdt)
+        x32 = xd.float().cpu().numpy()
+        lo, hi = regimes[trial % 4]
+        k = int(rng.integers(lo, min(hi, m) + 1))
+        if trial % 5 == 4:
+            mode, mi, cap = "early", int(rng.integers(1, 9)), 64
+        else:
+            mode, mi, cap = "exact", 4, int(rng.choice([1, 2, 3, 4, 5, 6, 8, 12, 64, 64, 64]))
+        want = oracle_lib.ref_batch(x32, k, mode, max_iter=mi, hard_cap=cap)
+        res = rtk.batch_topk(xd, rtk.BatchConfig(k=k, search=_search(mode, mi, 0.0, cap)))
+        ctx = (dtype, trial, n, m, k, mode, mi, cap)
+        assert np.array_equal(_np(res.indices), want[1]), ctx
+        assert np.array_equal(_bits(_np(res.values)), _bits(want[0])), ctx
