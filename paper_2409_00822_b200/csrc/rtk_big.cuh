@@ -111,13 +111,16 @@ __global__ void __launch_bounds__(BigThreads<E>::value, BigMinCtas<E, MASKED>::v
 // Paired long rows through the cp.async ring (E = 12..32 incl. masked rows,
 // where the TMA map does not apply): two ring slots per warp, refilled with
 // the next pair once both tiles are in registers; same pair scheme as above.
-template <int E, class In>
-struct BigPairCpMinCtas {  // 16-bit rows need the widening registers too: 128 registers
-    static constexpr int value = (E <= 16 && std::is_same<In, float>::value) ? 4 : 2;
+// fp32 E <= 16: 4 CTAs (64 registers), except exact mode at E = 16, where 3
+// (80 registers, no candidate-search spills) measured 3% faster (and 2-3%
+// slower at E = 12).  16-bit rows need the widening registers too: 128.
+template <int MODE, int E, class In>
+struct BigPairCpMinCtas {
+    static constexpr int value = (E <= 16 && std::is_same<In, float>::value) ? (MODE == kExact && E == 16 ? 3 : 4) : 2;
 };
 
 template <int MODE, int E, bool MASKED, class In = float, int CMAX = 4>
-__global__ void __launch_bounds__(RTK_BIG_THREADS, BigPairCpMinCtas<E, In>::value) rowtopk_big_pair_kernel(Args a) {
+__global__ void __launch_bounds__(RTK_BIG_THREADS, BigPairCpMinCtas<MODE, E, In>::value) rowtopk_big_pair_kernel(Args a) {
     using Row = LaneRowCut<E, MASKED>;
     constexpr bool kF32 = std::is_same<In, float>::value;
     constexpr unsigned kSlot = kF32 ? Row::kRowBytes : Row::kRowBytes16;
@@ -303,13 +306,17 @@ __device__ __forceinline__ void tma_pair(unsigned slotA, unsigned slotB, const C
     tma_row_noarrive(slotB, map, rowB, bar);
 }
 
-template <int E>
-struct BigPairMinCtas {  // E = 16: 64 registers (4 CTAs of 8 warps); E = 32: two 32-float tiles need ~100
-    static constexpr int value = E <= 16 ? 4 : 2;
+// E = 16: 4 CTAs of 8 warps (64 registers) in early-stop mode, 3 (80
+// registers) in exact mode, where the candidate-set search spilled at 64
+// (measured 1.5-2.3% faster; early stop equal); E = 32: two 32-float tiles
+// need ~100 registers.
+template <int MODE, int E>
+struct BigPairMinCtas {
+    static constexpr int value = E <= 16 ? (MODE == kExact ? 3 : 4) : 2;
 };
 
 template <int MODE, int E, int CMAX = 4>
-__global__ void __launch_bounds__(RTK_BIG_THREADS, BigPairMinCtas<E>::value) rowtopk_big_pair_tma_kernel(Args a,
+__global__ void __launch_bounds__(RTK_BIG_THREADS, BigPairMinCtas<MODE, E>::value) rowtopk_big_pair_tma_kernel(Args a,
                                                                                 const __grid_constant__ CUtensorMap map) {
     using Row = TmaRow<E>;
     extern __shared__ __align__(16) float smem[];
