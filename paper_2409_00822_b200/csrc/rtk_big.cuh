@@ -197,15 +197,41 @@ __global__ void __launch_bounds__(RTK_BIG_THREADS, BigPairCpMinCtas<MODE, E, In>
 
 namespace rtk {
 
+// E = 24 (paired kernel only): each lane's 24 floats come as two tensor
+// copies, elements 0..15 (64 B per lane, 64B swizzle) into the first 2 KB of
+// the slot and 16..23 (32 B per lane, 32B swizzle: chunk c of lane l at
+// c ^ ((l >> 2) & 1)) into the last 1 KB -- no swizzle applies to 96-byte
+// lane rows as a whole.
 template <int E>
 struct TmaRow : LaneRowCut<E, false> {
-    static_assert(E == 16 || E == 32, "TMA rows: E = 16 (64B swizzle) or 32 (128B swizzle)");
+    static_assert(E == 16 || E == 24 || E == 32, "TMA rows: E = 16 (64B swizzle), 24 (16 + 8) or 32 (128B swizzle)");
     static constexpr unsigned kSlotBytes = 32u * E * 4u;   // raw row, swizzled in place
     static constexpr unsigned kSlotAlign = E == 32 ? 1024u : 512u;
+    static constexpr unsigned kPart8 = 32u * 16u * 4u;  // E = 24: offset of the 8-float parts
     __device__ __forceinline__ static unsigned phys_chunk(int l, int c) {
         return E == 32 ? (unsigned)(c ^ (l & 7)) : (unsigned)(c ^ ((l >> 1) & 3));
     }
     __device__ __forceinline__ void load_swizzled(unsigned slot, int lane) {
+        if constexpr (E == 24) {
+            const unsigned b16 = slot + (unsigned)lane * 64u, b8 = slot + kPart8 + (unsigned)lane * 32u;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const float4 q = lds128(b16 + 16u * (unsigned)(c ^ ((lane >> 1) & 3)));
+                this->v[4 * c] = q.x;
+                this->v[4 * c + 1] = q.y;
+                this->v[4 * c + 2] = q.z;
+                this->v[4 * c + 3] = q.w;
+            }
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const float4 q = lds128(b8 + 16u * (unsigned)(c ^ ((lane >> 2) & 1)));
+                this->v[16 + 4 * c] = q.x;
+                this->v[16 + 4 * c + 1] = q.y;
+                this->v[16 + 4 * c + 2] = q.z;
+                this->v[16 + 4 * c + 3] = q.w;
+            }
+            return;
+        }
         const unsigned base = slot + (unsigned)lane * E * 4u;
 #pragma unroll
         for (int c = 0; c < E / 4; ++c) {
@@ -305,6 +331,17 @@ __device__ __forceinline__ void tma_pair(unsigned slotA, unsigned slotB, const C
     tma_row_noarrive(slotA, map, rowA, bar);
     tma_row_noarrive(slotB, map, rowB, bar);
 }
+// both rows' slots of a pair; E = 24: two copies per row (map: elements
+// 0..15 of every lane, map8: 16..23)
+template <int E>
+__device__ __forceinline__ void tma_pair_rows(unsigned slotA, unsigned slotB, const CUtensorMap* map,
+                                              const CUtensorMap* map8, int rowA, int rowB, unsigned bar) {
+    tma_pair(slotA, slotB, map, rowA, rowB, bar, TmaRow<E>::kSlotBytes);
+    if constexpr (E == 24) {
+        tma_row_noarrive(slotA + TmaRow<E>::kPart8, map8, rowA, bar);
+        tma_row_noarrive(slotB + TmaRow<E>::kPart8, map8, rowB, bar);
+    }
+}
 
 // E = 16: 4 CTAs of 8 warps (64 registers) in early-stop mode, 3 (80
 // registers) in exact mode, where the candidate-set search spilled at 64
@@ -316,8 +353,9 @@ struct BigPairMinCtas {
 };
 
 template <int MODE, int E, int CMAX = 4>
-__global__ void __launch_bounds__(RTK_BIG_THREADS, BigPairMinCtas<MODE, E>::value) rowtopk_big_pair_tma_kernel(Args a,
-                                                                                const __grid_constant__ CUtensorMap map) {
+__global__ void __launch_bounds__(RTK_BIG_THREADS, BigPairMinCtas<MODE, E>::value)
+    rowtopk_big_pair_tma_kernel(Args a, const __grid_constant__ CUtensorMap map,
+                                const __grid_constant__ CUtensorMap map8) {  // map8: E = 24 only
     using Row = TmaRow<E>;
     extern __shared__ __align__(16) float smem[];
     const int lane = threadIdx.x & 31;
@@ -340,7 +378,7 @@ __global__ void __launch_bounds__(RTK_BIG_THREADS, BigPairMinCtas<MODE, E>::valu
     if (lane == 0) {
         mbar_init(bar);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        tma_pair(slotA, slotB, &map, (int)r, (int)min(r + nw, last), bar, Row::kSlotBytes);
+        tma_pair_rows<E>(slotA, slotB, &map, &map8, (int)r, (int)min(r + nw, last), bar);
     }
     __syncwarp();
     unsigned phase = 0;
@@ -355,8 +393,8 @@ __global__ void __launch_bounds__(RTK_BIG_THREADS, BigPairMinCtas<MODE, E>::valu
             __syncwarp();  // every lane has read both slots
             if (lane == 0 && rn < n) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                tma_pair(slotA, slotB, &map, (int)(rn + (tok & a.opaque_zero)), (int)min(rn + nw, last), bar,
-                         Row::kSlotBytes);
+                tma_pair_rows<E>(slotA, slotB, &map, &map8, (int)(rn + (tok & a.opaque_zero)), (int)min(rn + nw, last),
+                                 bar);
             }
         });
         if (rn >= n) break;

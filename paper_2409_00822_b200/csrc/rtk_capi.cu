@@ -213,6 +213,31 @@ bool rtk_encode_row_map(CUtensorMap* map, const float* x, long long n, int e, lo
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
+// 768-column rows as [n][32][24]: lanes' elements 0..15 (64B swizzle) and
+// 16..23 (32B swizzle) as two maps over the same rows (TmaRow<24>).
+bool rtk_encode_row_map24(CUtensorMap* map16, CUtensorMap* map8, const float* x, long long n, long long ldx) {
+    CUtensorMap probe;
+    if (!rtk_encode_row_map(&probe, x, n, 16, ldx)) return false;  // entry point + alignment checks
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return false;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t strides[2] = {24 * 4, (cuuint64_t)ldx * 4};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const cuuint64_t d16[3] = {16, 32, (cuuint64_t)n}, d8[3] = {8, 32, (cuuint64_t)n};
+    const cuuint32_t b16[3] = {16, 32, 1}, b8[3] = {8, 32, 1};
+    return encode(map16, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(x), d16, strides, b16, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS &&
+           encode(map8, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(x + 16), d8, strides, b8, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 int rtk_ctas_per_sm(const void* kernel, size_t smem, int threads) { return ctas_per_sm(kernel, smem, threads); }
 
 extern "C" {

@@ -28,6 +28,7 @@ int rtk_describe_exact(const rtk::Args& a, int* shape3);
 int rtk_describe_early(const rtk::Args& a, int* shape3);
 int rtk_describe_trace(const rtk::Args& a, int* shape3);
 bool rtk_encode_row_map(CUtensorMap* map, const float* x, long long n, int e, long long ldx);
+bool rtk_encode_row_map24(CUtensorMap* map16, CUtensorMap* map8, const float* x, long long n, long long ldx);
 
 namespace rtk_dispatch {
 
@@ -138,9 +139,9 @@ int launch_big_tma_kernel(const rtk::Args& a, cudaStream_t s, const CUtensorMap&
 // Paired long rows on TMA slots (rtk_big.cuh): E = 16, no traces, exact
 // with eps_rel = 0 or early stop.
 template <int MODE, int E, int CMAX = 4>
-int launch_big_pair_tma_kernel(const rtk::Args& a, cudaStream_t s, const CUtensorMap& map) {
+int launch_big_pair_tma_kernel(const rtk::Args& a, cudaStream_t s, const CUtensorMap& map, const CUtensorMap& map8) {
     if constexpr (CMAX == 4 && MODE == rtk::kExact && E >= 24) {  // the 8-slot candidate search, own kernel
-        if (rtk::long_cand8<E>(a.k)) return launch_big_pair_tma_kernel<MODE, E, 8>(a, s, map);
+        if (rtk::long_cand8<E>(a.k)) return launch_big_pair_tma_kernel<MODE, E, 8>(a, s, map, map8);
     }
     using Row = rtk::TmaRow<E>;
     constexpr int wpc = RTK_BIG_THREADS / 32;
@@ -153,7 +154,7 @@ int launch_big_pair_tma_kernel(const rtk::Args& a, cudaStream_t s, const CUtenso
                                                                    RTK_BIG_THREADS);
     if (grid > blocks_needed) grid = blocks_needed;
     if (grid < 1) grid = 1;
-    kernel<<<(unsigned)grid, RTK_BIG_THREADS, smem, s>>>(a, map);
+    kernel<<<(unsigned)grid, RTK_BIG_THREADS, smem, s>>>(a, map, map8);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(RTK_ECUDA, "kernel launch failed: %s", cudaGetErrorString(e));
     return RTK_OK;
@@ -182,8 +183,16 @@ bool big_pair_eligible(const rtk::Args& a) {
            (MODE == rtk::kEarly ? a.k < 128 : a.eps_rel == 0.0);
 }
 
+#ifndef RTK_TMA_E24
+#define RTK_TMA_E24 1
+#endif
 template <int MODE, int E, bool MASKED>
 int launch_big(const rtk::Args& a, cudaStream_t s) {
+    if constexpr (RTK_USE_TMA && RTK_BIG_PAIR && RTK_TMA_E24 && !MASKED && E == 24 && MODE != rtk::kTrace) {
+        CUtensorMap m16, m8;  // paired rows only: two tensor copies per row (TmaRow<24>)
+        if (big_pair_eligible<MODE>(a) && a.n < (1LL << 31) && rtk_encode_row_map24(&m16, &m8, a.x, a.n, a.ldx))
+            return launch_big_pair_tma_kernel<MODE, E>(a, s, m16, m8);
+    }
     if constexpr (RTK_USE_TMA && !MASKED && (E == 16 || E == 32)) {
         CUtensorMap map;
         if (a.n < (1LL << 31) && rtk_encode_row_map(&map, a.x, a.n, E, a.ldx)) {
@@ -191,7 +200,7 @@ int launch_big(const rtk::Args& a, cudaStream_t s) {
 #define RTK_BIG_PAIR_E32 1
 #endif
             if constexpr (RTK_BIG_PAIR && (E == 16 || (RTK_BIG_PAIR_E32 && E == 32)) && MODE != rtk::kTrace) {
-                if (big_pair_eligible<MODE>(a)) return launch_big_pair_tma_kernel<MODE, E>(a, s, map);
+                if (big_pair_eligible<MODE>(a)) return launch_big_pair_tma_kernel<MODE, E>(a, s, map, map);
             }
             if constexpr (MODE == rtk::kTrace) {
                 return launch_big_tma_kernel<MODE, E, true>(a, s, map);
