@@ -17,12 +17,12 @@ import paper_2409_00822_b200 as rtk  # noqa: E402
 
 def main():
     rng = np.random.default_rng(0)
-    for m in (4, 8, 100, 128, 256, 257, 384, 512, 777, 1024, 1500, 2048, 2500, 3072, 4000, 4500, 6144, 8192):
+    for m in (4, 8, 100, 128, 256, 257, 384, 512, 768, 777, 1024, 1500, 2048, 2500, 3072, 4000, 4500, 6144, 8192):
         n = 67 if m <= 1024 else 19
         x = rng.standard_normal((n, m), dtype=np.float32)
         x[5] = 1.0
         x[9, : m // 2] = np.inf
-        for k in sorted({1, min(33, m), m}):
+        for k in sorted({1, min(33, m), m} | ({70, 150} if 512 <= m <= 1024 else set())):  # + candidate sets
             for search, mode, mi in ((rtk.SearchConfig.exact(), "exact", 4), (rtk.SearchConfig.early_stop(3), "early", 3)):
                 v, i, t, r = oracle.ref_batch(x, k, mode, max_iter=mi)
                 for traces in (False, True):
