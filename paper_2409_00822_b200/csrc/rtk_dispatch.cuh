@@ -176,11 +176,13 @@ int launch_big_pair_kernel(const rtk::Args& a, cudaStream_t s) {
     return launch_rows(rtk::rowtopk_big_pair_kernel<MODE, E, MASKED, float, CMAX>, a, s, (size_t)wpc * per_warp, RTK_BIG_THREADS, 2);
 }
 
-template <int MODE>
+// Early stop with k >= 128 stays on the single-row kernel at E <= 16 (two
+// k-pair flushes per step measured 5-6% slower paired there); from E = 20 up
+// the paired kernel is faster (M = 768: -13%, M = 640 / 1024: -2..3%).
+template <int MODE, int E>
 bool big_pair_eligible(const rtk::Args& a) {
-    // early stop with k >= 128 measured 6% slower paired (two k-pair flushes per step)
     return MODE != rtk::kTrace && a.iters == nullptr && a.reasons == nullptr && a.n < (1LL << 30) &&
-           (MODE == rtk::kEarly ? a.k < 128 : a.eps_rel == 0.0);
+           (MODE == rtk::kEarly ? (a.k < 128 || E > 16) : a.eps_rel == 0.0);
 }
 
 #ifndef RTK_TMA_E24
@@ -190,7 +192,7 @@ template <int MODE, int E, bool MASKED>
 int launch_big(const rtk::Args& a, cudaStream_t s) {
     if constexpr (RTK_USE_TMA && RTK_BIG_PAIR && RTK_TMA_E24 && !MASKED && E == 24 && MODE != rtk::kTrace) {
         CUtensorMap m16, m8;  // paired rows only: two tensor copies per row (TmaRow<24>)
-        if (big_pair_eligible<MODE>(a) && a.n < (1LL << 31) && rtk_encode_row_map24(&m16, &m8, a.x, a.n, a.ldx))
+        if (big_pair_eligible<MODE, E>(a) && a.n < (1LL << 31) && rtk_encode_row_map24(&m16, &m8, a.x, a.n, a.ldx))
             return launch_big_pair_tma_kernel<MODE, E>(a, s, m16, m8);
     }
     if constexpr (RTK_USE_TMA && !MASKED && (E == 16 || E == 32)) {
@@ -200,7 +202,7 @@ int launch_big(const rtk::Args& a, cudaStream_t s) {
 #define RTK_BIG_PAIR_E32 1
 #endif
             if constexpr (RTK_BIG_PAIR && (E == 16 || (RTK_BIG_PAIR_E32 && E == 32)) && MODE != rtk::kTrace) {
-                if (big_pair_eligible<MODE>(a)) return launch_big_pair_tma_kernel<MODE, E>(a, s, map, map);
+                if (big_pair_eligible<MODE, E>(a)) return launch_big_pair_tma_kernel<MODE, E>(a, s, map, map);
             }
             if constexpr (MODE == rtk::kTrace) {
                 return launch_big_tma_kernel<MODE, E, true>(a, s, map);
@@ -213,7 +215,7 @@ int launch_big(const rtk::Args& a, cudaStream_t s) {
         }
     }
     if constexpr (RTK_BIG_PAIR_CP && E <= 32 && MODE != rtk::kTrace) {
-        if (big_pair_eligible<MODE>(a)) return launch_big_pair_kernel<MODE, E, MASKED>(a, s);
+        if (big_pair_eligible<MODE, E>(a)) return launch_big_pair_kernel<MODE, E, MASKED>(a, s);
     }
     if constexpr (MODE == rtk::kTrace) {
         return launch_big_kernel<MODE, E, MASKED, true>(a, s);

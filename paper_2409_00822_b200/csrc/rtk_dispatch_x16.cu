@@ -45,7 +45,7 @@ template <int MODE, int E, class In>
 int launch_big16(const rtk::Args& a, cudaStream_t s) {
     // (paired 16-bit tiles spill above E = 20 even at 128 registers: E <= 20 only)
     if constexpr (RTK_BIG_PAIR_CP && E <= 20) {
-        if (rtk_dispatch::big_pair_eligible<MODE>(a)) {
+        if (rtk_dispatch::big_pair_eligible<MODE, E>(a)) {
             if (a.m == 32 * E) return launch_big16_pair_kernel<MODE, E, false, In>(a, s);
             return launch_big16_pair_kernel<MODE, E, true, In>(a, s);
         }

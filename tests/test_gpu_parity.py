@@ -450,10 +450,10 @@ def test_launch_shape_describes_the_dispatch():
     for m in (384, 500, 512, 768, 1000, 1024, 2048, 4096):
         w, c, r = shape(m, 64, 0)
         # up to 1024 columns: paired long rows (TMA slots for M = 512 / 1024, the
-        # cp.async ring otherwise; exact, and early stop for k < 128)
+        # cp.async ring otherwise; exact, and early stop for k < 128 or M > 512)
         assert r == (2 if m <= 1024 else 1) and w >= 1 and c >= 1, (m, w, c, r)
     assert shape(512, 64, 1)[2] == 2 and shape(512, 128, 1)[2] == 1 and shape(512, 64, 2)[2] == 1
-    assert shape(1024, 32, 1)[2] == 2 and shape(768, 128, 1)[2] == 1
+    assert shape(1024, 32, 1)[2] == 2 and shape(768, 128, 1)[2] == 2  # early stop, k >= 128: paired above E = 16
     assert shape(8192, 64, 0)[::2] == (2, 0) and shape(8192, 64, 1)[::2] == (4, 0)  # CTA per row
     assert shape(3000, 2999, 1)[0] < 8                                    # large k: fewer warps per CTA
     assert shape(128, 128, 0) == (8, 0, 0)                                # k == M copy
