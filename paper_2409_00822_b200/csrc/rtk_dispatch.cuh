@@ -140,7 +140,7 @@ int launch_big_tma_kernel(const rtk::Args& a, cudaStream_t s, const CUtensorMap&
 // with eps_rel = 0 or early stop.
 template <int MODE, int E, int CMAX = 4>
 int launch_big_pair_tma_kernel(const rtk::Args& a, cudaStream_t s, const CUtensorMap& map, const CUtensorMap& map8) {
-    if constexpr (CMAX == 4 && MODE == rtk::kExact && E >= 24) {  // the 8-slot candidate search, own kernel
+    if constexpr (CMAX == 4 && MODE == rtk::kExact && E >= RTK_CAND8_MIN_E) {  // the 8-slot candidate search, own kernel
         if (rtk::long_cand8<E>(a.k)) return launch_big_pair_tma_kernel<MODE, E, 8>(a, s, map, map8);
     }
     using Row = rtk::TmaRow<E>;
@@ -167,7 +167,7 @@ int launch_big_pair_tma_kernel(const rtk::Args& a, cudaStream_t s, const CUtenso
 #endif
 template <int MODE, int E, bool MASKED, int CMAX = 4>
 int launch_big_pair_kernel(const rtk::Args& a, cudaStream_t s) {
-    if constexpr (CMAX == 4 && MODE == rtk::kExact && E >= 24) {  // the 8-slot candidate search
+    if constexpr (CMAX == 4 && MODE == rtk::kExact && E >= RTK_CAND8_MIN_E) {  // the 8-slot candidate search
         if (rtk::long_cand8<E>(a.k)) return launch_big_pair_kernel<MODE, E, MASKED, 8>(a, s);
     }
     using Row = rtk::LaneRowCut<E, MASKED>;

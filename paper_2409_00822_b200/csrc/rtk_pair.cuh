@@ -300,13 +300,16 @@ __device__ __forceinline__ void load_tile(Row& R, const Args& a, unsigned r, uns
 #ifndef RTK_LONG_CAND
 #define RTK_LONG_CAND 1
 #endif
-// candidate slots per lane: 2 (k <= 40), 4 (k <= 96), 8 (k <= 192; E >= 24
-// only, in a separate kernel instantiation (CMAX = 8): at E = 16 the staging
-// would cost occupancy and a candidate step would count half the tile, and
-// compiled into the k <= 96 kernels the third search raised their spills)
+// candidate slots per lane: 2 (k <= 40), 4 (k <= 96), 8 (k <= 192; E >= 16,
+// in a separate kernel instantiation (CMAX = 8): compiled into the k <= 96
+// kernels the third search raised their spills).  At E = 16 a candidate step
+// still counts half the tile, and measured 4-6% faster at M = 512.
+#ifndef RTK_CAND8_MIN_E
+#define RTK_CAND8_MIN_E 16
+#endif
 template <int E>
 __host__ __device__ constexpr bool long_cand8(int k) {
-    return E >= 24 && k > 96 && k <= 192;
+    return E >= RTK_CAND8_MIN_E && k > 96 && k <= 192;
 }
 // staging bytes per row of the paired long-row kernels: the k-pair staging
 // of LaneRowCut or the candidate set, whichever is larger

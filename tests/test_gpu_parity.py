@@ -574,7 +574,7 @@ def test_paired_long_rows_adversarial(oracle_lib, m):
 def test_long_row_candidate_search_boundaries(oracle_lib, m):
     """The candidate-set exact search of the paired long-row kernels at its
     boundaries: k around the 2-slot / 4-slot / 8-slot / off switches (40, 41,
-    96, 97, 192, 193; 8 slots on rows of 768+ columns, its own kernel),
+    96, 97, 192, 193; 8 slots from 16 elements per lane up, its own kernel),
     hard caps small enough to end the search in the full phase, at the switch
     to the candidate phase, or inside it (1..6), and normal rows whose
     candidate set is close to the capacity; bit-exact vs the oracle."""
