@@ -307,15 +307,21 @@ __device__ __forceinline__ void load_tile(Row& R, const Args& a, unsigned r, uns
 #ifndef RTK_CAND8_MIN_E
 #define RTK_CAND8_MIN_E 16
 #endif
+#ifndef RTK_CAND2_KMAX  // switch points measured against 52 / 96 and 32 / 72: best or equal on 12 shapes
+#define RTK_CAND2_KMAX 40
+#endif
+#ifndef RTK_CAND4_KMAX
+#define RTK_CAND4_KMAX 96
+#endif
 template <int E>
 __host__ __device__ constexpr bool long_cand8(int k) {
-    return E >= RTK_CAND8_MIN_E && k > 96 && k <= 192;
+    return E >= RTK_CAND8_MIN_E && k > RTK_CAND4_KMAX && k <= 192;
 }
 // staging bytes per row of the paired long-row kernels: the k-pair staging
 // of LaneRowCut or the candidate set, whichever is larger
 template <class Row>
 __host__ __device__ constexpr unsigned pair_stage_bytes(int k) {
-    const int slots = k <= 40 ? 2 : (k <= 96 ? 4 : (long_cand8<Row::kSlots>(k) ? 8 : 0));
+    const int slots = k <= RTK_CAND2_KMAX ? 2 : (k <= RTK_CAND4_KMAX ? 4 : (long_cand8<Row::kSlots>(k) ? 8 : 0));
     const unsigned cand = 8u * 32u * (unsigned)slots;
     return Row::stage_bytes(k) > cand ? Row::stage_bytes(k) : cand;
 }
@@ -580,12 +586,12 @@ __device__ __forceinline__ void process_pair_sel(const Row& A, const Row& B, uns
                 exact_pair_cand<8, In>(A, B, rA, rB, a, lane, sA, sB, steps, mnA, mxA, mnB, mxB, ovA, oiA, ovB, oiB);
                 return;
             } else {
-                if (k <= 40) {
+                if (k <= RTK_CAND2_KMAX) {
                     exact_pair_cand<2, In>(A, B, rA, rB, a, lane, sA, sB, steps, mnA, mxA, mnB, mxB, ovA, oiA, ovB,
                                            oiB);
                     return;
                 }
-                if (k <= 96) {
+                if (k <= RTK_CAND4_KMAX) {
                     exact_pair_cand<4, In>(A, B, rA, rB, a, lane, sA, sB, steps, mnA, mxA, mnB, mxB, ovA, oiA, ovB,
                                            oiB);
                     return;
