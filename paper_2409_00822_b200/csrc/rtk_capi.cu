@@ -192,7 +192,8 @@ int rtk_device_sms() { return device_sms(); }
 // Tensor map of x viewed as [n][32][e] floats (row stride ldx), box = one row,
 // swizzle matching the row width (128B for e = 32, 64B for e = 16).  The
 // driver entry point is fetched once through the runtime (no -lcuda).
-bool rtk_encode_row_map(CUtensorMap* map, const float* x, long long n, int e, long long ldx) {
+// cuTensorMapEncodeTiled through the runtime's driver entry point (resolved once)
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     static std::once_flag once;
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     std::call_once(once, [] {
@@ -202,6 +203,11 @@ bool rtk_encode_row_map(CUtensorMap* map, const float* x, long long n, int e, lo
             q == cudaDriverEntryPointSuccess)
             encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     });
+    return encode;
+}
+
+bool rtk_encode_row_map(CUtensorMap* map, const float* x, long long n, int e, long long ldx) {
+    const PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
     if (!encode || (reinterpret_cast<uintptr_t>(x) & 15) || (ldx * 4) % 16) return false;
     const cuuint64_t dims[3] = {(cuuint64_t)e, 32, (cuuint64_t)n};
     const cuuint64_t strides[2] = {(cuuint64_t)e * 4, (cuuint64_t)ldx * 4};
@@ -216,17 +222,8 @@ bool rtk_encode_row_map(CUtensorMap* map, const float* x, long long n, int e, lo
 // 768-column rows as [n][32][24]: lanes' elements 0..15 (64B swizzle) and
 // 16..23 (32B swizzle) as two maps over the same rows (TmaRow<24>).
 bool rtk_encode_row_map24(CUtensorMap* map16, CUtensorMap* map8, const float* x, long long n, long long ldx) {
-    CUtensorMap probe;
-    if (!rtk_encode_row_map(&probe, x, n, 16, ldx)) return false;  // entry point + alignment checks
-    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-    if (!encode) {
-        void* fn = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            return false;
-        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    }
+    const PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
+    if (!encode || (reinterpret_cast<uintptr_t>(x) & 15) || (ldx * 4) % 16) return false;
     const cuuint64_t strides[2] = {24 * 4, (cuuint64_t)ldx * 4};
     const cuuint32_t estr[3] = {1, 1, 1};
     const cuuint64_t d16[3] = {16, 32, (cuuint64_t)n}, d8[3] = {8, 32, (cuuint64_t)n};
