@@ -197,39 +197,58 @@ __global__ void __launch_bounds__(RTK_BIG_THREADS, BigPairCpMinCtas<MODE, E, In>
 
 namespace rtk {
 
-// E = 24 (paired kernel only): each lane's 24 floats come as two tensor
-// copies, elements 0..15 (64 B per lane, 64B swizzle) into the first 2 KB of
-// the slot and 16..23 (32 B per lane, 32B swizzle: chunk c of lane l at
-// c ^ ((l >> 2) & 1)) into the last 1 KB -- no swizzle applies to 96-byte
-// lane rows as a whole.
+// Split widths (paired kernel only): lane rows of 48-112 bytes fit no
+// swizzle, so each row arrives as up to three tensor copies of 16 / 8 / 4
+// floats per lane -- 16 with 64B swizzle, 8 with 32B swizzle (chunk c of
+// lane l at c ^ ((l >> 2) & 1)), 4 unswizzled -- into consecutive parts of
+// the slot.
+template <int E>
+struct TmaParts {
+    // E = 24 only: the 4-float parts of E = 12 / 20 / 28 (16-byte boxes)
+    // measured 4-7% slower in exact mode and 26-33% slower in early stop than
+    // the cp.async ring
+    static constexpr bool kSplit = E == 24;
+    static constexpr int w0 = kSplit ? (E >= 16 ? 16 : 8) : E;
+    static constexpr int w1 = kSplit ? (E >= 16 ? ((E - 16) >= 8 ? 8 : E - 16) : E - 8) : 0;
+    static constexpr int w2 = kSplit ? E - w0 - w1 : 0;
+    static constexpr int n = 1 + (w1 > 0) + (w2 > 0);
+    __host__ __device__ static constexpr int width(int i) { return i == 0 ? w0 : (i == 1 ? w1 : w2); }
+    __host__ __device__ static constexpr int first(int i) { return i == 0 ? 0 : (i == 1 ? w0 : w0 + w1); }
+    static_assert(!kSplit || ((w1 == 0 || w1 == 8 || w1 == 4) && (w2 == 0 || w2 == 4)), "split TMA rows: 16 / 8 / 4 parts");
+};
+
 template <int E>
 struct TmaRow : LaneRowCut<E, false> {
-    static_assert(E == 16 || E == 24 || E == 32, "TMA rows: E = 16 (64B swizzle), 24 (16 + 8) or 32 (128B swizzle)");
+    using Parts = TmaParts<E>;
     static constexpr unsigned kSlotBytes = 32u * E * 4u;   // raw row, swizzled in place
     static constexpr unsigned kSlotAlign = E == 32 ? 1024u : 512u;
-    static constexpr unsigned kPart8 = 32u * 16u * 4u;  // E = 24: offset of the 8-float parts
     __device__ __forceinline__ static unsigned phys_chunk(int l, int c) {
         return E == 32 ? (unsigned)(c ^ (l & 7)) : (unsigned)(c ^ ((l >> 1) & 3));
     }
+    template <int W>
+    __device__ __forceinline__ static unsigned part_chunk(int l, int c) {
+        return W == 16 ? (unsigned)(c ^ ((l >> 1) & 3)) : (W == 8 ? (unsigned)(c ^ ((l >> 2) & 1)) : (unsigned)c);
+    }
+    template <int P>
+    __device__ __forceinline__ void load_part(unsigned slot, int lane) {
+        constexpr int W = Parts::width(P), Q = Parts::first(P);
+        if constexpr (W > 0) {
+            const unsigned b = slot + 32u * 4u * (unsigned)Q + (unsigned)lane * 4u * W;
+#pragma unroll
+            for (int c = 0; c < W / 4; ++c) {
+                const float4 q = lds128(b + 16u * part_chunk<W>(lane, c));
+                this->v[Q + 4 * c] = q.x;
+                this->v[Q + 4 * c + 1] = q.y;
+                this->v[Q + 4 * c + 2] = q.z;
+                this->v[Q + 4 * c + 3] = q.w;
+            }
+        }
+    }
     __device__ __forceinline__ void load_swizzled(unsigned slot, int lane) {
-        if constexpr (E == 24) {
-            const unsigned b16 = slot + (unsigned)lane * 64u, b8 = slot + kPart8 + (unsigned)lane * 32u;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const float4 q = lds128(b16 + 16u * (unsigned)(c ^ ((lane >> 1) & 3)));
-                this->v[4 * c] = q.x;
-                this->v[4 * c + 1] = q.y;
-                this->v[4 * c + 2] = q.z;
-                this->v[4 * c + 3] = q.w;
-            }
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const float4 q = lds128(b8 + 16u * (unsigned)(c ^ ((lane >> 2) & 1)));
-                this->v[16 + 4 * c] = q.x;
-                this->v[16 + 4 * c + 1] = q.y;
-                this->v[16 + 4 * c + 2] = q.z;
-                this->v[16 + 4 * c + 3] = q.w;
-            }
+        if constexpr (Parts::kSplit) {
+            load_part<0>(slot, lane);
+            load_part<1>(slot, lane);
+            load_part<2>(slot, lane);
             return;
         }
         const unsigned base = slot + (unsigned)lane * E * 4u;
@@ -331,15 +350,23 @@ __device__ __forceinline__ void tma_pair(unsigned slotA, unsigned slotB, const C
     tma_row_noarrive(slotA, map, rowA, bar);
     tma_row_noarrive(slotB, map, rowB, bar);
 }
-// both rows' slots of a pair; E = 24: two copies per row (map: elements
-// 0..15 of every lane, map8: 16..23)
+// both rows' slots of a pair: one tensor copy per row, or one per part
+// (maps[0..2]) for the split widths
 template <int E>
-__device__ __forceinline__ void tma_pair_rows(unsigned slotA, unsigned slotB, const CUtensorMap* map,
-                                              const CUtensorMap* map8, int rowA, int rowB, unsigned bar) {
-    tma_pair(slotA, slotB, map, rowA, rowB, bar, TmaRow<E>::kSlotBytes);
-    if constexpr (E == 24) {
-        tma_row_noarrive(slotA + TmaRow<E>::kPart8, map8, rowA, bar);
-        tma_row_noarrive(slotB + TmaRow<E>::kPart8, map8, rowB, bar);
+__device__ __forceinline__ void tma_pair_rows(unsigned slotA, unsigned slotB, const CUtensorMap* m0,
+                                              const CUtensorMap* m1, const CUtensorMap* m2, int rowA, int rowB,
+                                              unsigned bar) {
+    using Parts = TmaParts<E>;
+    tma_pair(slotA, slotB, m0, rowA, rowB, bar, TmaRow<E>::kSlotBytes);
+    if constexpr (Parts::w1 > 0) {
+        constexpr unsigned off = 32u * 4u * Parts::first(1);
+        tma_row_noarrive(slotA + off, m1, rowA, bar);
+        tma_row_noarrive(slotB + off, m1, rowB, bar);
+    }
+    if constexpr (Parts::w2 > 0) {
+        constexpr unsigned off = 32u * 4u * Parts::first(2);
+        tma_row_noarrive(slotA + off, m2, rowA, bar);
+        tma_row_noarrive(slotB + off, m2, rowB, bar);
     }
 }
 
@@ -349,13 +376,14 @@ __device__ __forceinline__ void tma_pair_rows(unsigned slotA, unsigned slotB, co
 // need ~100 registers.
 template <int MODE, int E>
 struct BigPairMinCtas {
-    static constexpr int value = E <= 16 ? (MODE == kExact ? 3 : 4) : 2;
+    static constexpr int value = E == 16 ? (MODE == kExact ? 3 : 4) : (E < 16 ? 4 : 2);
 };
 
 template <int MODE, int E, int CMAX = 4>
 __global__ void __launch_bounds__(RTK_BIG_THREADS, BigPairMinCtas<MODE, E>::value)
     rowtopk_big_pair_tma_kernel(Args a, const __grid_constant__ CUtensorMap map,
-                                const __grid_constant__ CUtensorMap map8) {  // map8: E = 24 only
+                                const __grid_constant__ CUtensorMap map1,  // split widths: parts 1 and 2
+                                const __grid_constant__ CUtensorMap map2) {
     using Row = TmaRow<E>;
     extern __shared__ __align__(16) float smem[];
     const int lane = threadIdx.x & 31;
@@ -378,7 +406,7 @@ __global__ void __launch_bounds__(RTK_BIG_THREADS, BigPairMinCtas<MODE, E>::valu
     if (lane == 0) {
         mbar_init(bar);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        tma_pair_rows<E>(slotA, slotB, &map, &map8, (int)r, (int)min(r + nw, last), bar);
+        tma_pair_rows<E>(slotA, slotB, &map, &map1, &map2, (int)r, (int)min(r + nw, last), bar);
     }
     __syncwarp();
     unsigned phase = 0;
@@ -393,8 +421,8 @@ __global__ void __launch_bounds__(RTK_BIG_THREADS, BigPairMinCtas<MODE, E>::valu
             __syncwarp();  // every lane has read both slots
             if (lane == 0 && rn < n) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                tma_pair_rows<E>(slotA, slotB, &map, &map8, (int)(rn + (tok & a.opaque_zero)), (int)min(rn + nw, last),
-                                 bar);
+                tma_pair_rows<E>(slotA, slotB, &map, &map1, &map2, (int)(rn + (tok & a.opaque_zero)),
+                                 (int)min(rn + nw, last), bar);
             }
         });
         if (rn >= n) break;

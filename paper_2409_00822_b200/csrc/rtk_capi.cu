@@ -219,21 +219,29 @@ bool rtk_encode_row_map(CUtensorMap* map, const float* x, long long n, int e, lo
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
-// 768-column rows as [n][32][24]: lanes' elements 0..15 (64B swizzle) and
-// 16..23 (32B swizzle) as two maps over the same rows (TmaRow<24>).
-bool rtk_encode_row_map24(CUtensorMap* map16, CUtensorMap* map8, const float* x, long long n, long long ldx) {
+// Lane rows of E floats as [n][32][E] split into parts of 16 / 8 / 4 floats
+// (TmaRow): part p covers elements first(p) .. first(p) + widths[p] of every
+// lane, 64B / 32B / no swizzle.
+bool rtk_encode_row_parts(CUtensorMap* maps, const float* x, long long n, int e, long long ldx, const int* widths,
+                          int parts) {
     const PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
-    if (!encode || (reinterpret_cast<uintptr_t>(x) & 15) || (ldx * 4) % 16) return false;
-    const cuuint64_t strides[2] = {24 * 4, (cuuint64_t)ldx * 4};
+    if (!encode || (reinterpret_cast<uintptr_t>(x) & 15) || (ldx * 4) % 16 || (e * 4) % 16) return false;
+    const cuuint64_t strides[2] = {(cuuint64_t)e * 4, (cuuint64_t)ldx * 4};
     const cuuint32_t estr[3] = {1, 1, 1};
-    const cuuint64_t d16[3] = {16, 32, (cuuint64_t)n}, d8[3] = {8, 32, (cuuint64_t)n};
-    const cuuint32_t b16[3] = {16, 32, 1}, b8[3] = {8, 32, 1};
-    return encode(map16, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(x), d16, strides, b16, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS &&
-           encode(map8, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(x + 16), d8, strides, b8, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    int first = 0;
+    for (int p = 0; p < parts; ++p) {
+        const int w = widths[p];
+        const cuuint64_t dims[3] = {(cuuint64_t)w, 32, (cuuint64_t)n};
+        const cuuint32_t box[3] = {(cuuint32_t)w, 32, 1};
+        const CUtensorMapSwizzle sw =
+            w == 16 ? CU_TENSOR_MAP_SWIZZLE_64B : (w == 8 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE);
+        if (encode(&maps[p], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(x + first), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+        first += w;
+    }
+    return true;
 }
 int rtk_ctas_per_sm(const void* kernel, size_t smem, int threads) { return ctas_per_sm(kernel, smem, threads); }
 

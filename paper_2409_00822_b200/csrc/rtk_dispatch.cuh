@@ -28,7 +28,8 @@ int rtk_describe_exact(const rtk::Args& a, int* shape3);
 int rtk_describe_early(const rtk::Args& a, int* shape3);
 int rtk_describe_trace(const rtk::Args& a, int* shape3);
 bool rtk_encode_row_map(CUtensorMap* map, const float* x, long long n, int e, long long ldx);
-bool rtk_encode_row_map24(CUtensorMap* map16, CUtensorMap* map8, const float* x, long long n, long long ldx);
+bool rtk_encode_row_parts(CUtensorMap* maps, const float* x, long long n, int e, long long ldx, const int* widths,
+                          int parts);
 
 namespace rtk_dispatch {
 
@@ -139,9 +140,10 @@ int launch_big_tma_kernel(const rtk::Args& a, cudaStream_t s, const CUtensorMap&
 // Paired long rows on TMA slots (rtk_big.cuh): E = 16, no traces, exact
 // with eps_rel = 0 or early stop.
 template <int MODE, int E, int CMAX = 4>
-int launch_big_pair_tma_kernel(const rtk::Args& a, cudaStream_t s, const CUtensorMap& map, const CUtensorMap& map8) {
+int launch_big_pair_tma_kernel(const rtk::Args& a, cudaStream_t s, const CUtensorMap& map, const CUtensorMap& map1,
+                               const CUtensorMap& map2) {
     if constexpr (CMAX == 4 && MODE == rtk::kExact && E >= RTK_CAND8_MIN_E) {  // the 8-slot candidate search, own kernel
-        if (rtk::long_cand8<E>(a.k)) return launch_big_pair_tma_kernel<MODE, E, 8>(a, s, map, map8);
+        if (rtk::long_cand8<E>(a.k)) return launch_big_pair_tma_kernel<MODE, E, 8>(a, s, map, map1, map2);
     }
     using Row = rtk::TmaRow<E>;
     constexpr int wpc = RTK_BIG_THREADS / 32;
@@ -154,7 +156,7 @@ int launch_big_pair_tma_kernel(const rtk::Args& a, cudaStream_t s, const CUtenso
                                                                    RTK_BIG_THREADS);
     if (grid > blocks_needed) grid = blocks_needed;
     if (grid < 1) grid = 1;
-    kernel<<<(unsigned)grid, RTK_BIG_THREADS, smem, s>>>(a, map, map8);
+    kernel<<<(unsigned)grid, RTK_BIG_THREADS, smem, s>>>(a, map, map1, map2);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(RTK_ECUDA, "kernel launch failed: %s", cudaGetErrorString(e));
     return RTK_OK;
@@ -185,15 +187,19 @@ bool big_pair_eligible(const rtk::Args& a) {
            (MODE == rtk::kEarly ? (a.k < 128 || E > 16) : a.eps_rel == 0.0);
 }
 
-#ifndef RTK_TMA_E24
-#define RTK_TMA_E24 1
+#ifndef RTK_TMA_SPLIT
+#define RTK_TMA_SPLIT 1
 #endif
 template <int MODE, int E, bool MASKED>
 int launch_big(const rtk::Args& a, cudaStream_t s) {
-    if constexpr (RTK_USE_TMA && RTK_BIG_PAIR && RTK_TMA_E24 && !MASKED && E == 24 && MODE != rtk::kTrace) {
-        CUtensorMap m16, m8;  // paired rows only: two tensor copies per row (TmaRow<24>)
-        if (big_pair_eligible<MODE, E>(a) && a.n < (1LL << 31) && rtk_encode_row_map24(&m16, &m8, a.x, a.n, a.ldx))
-            return launch_big_pair_tma_kernel<MODE, E>(a, s, m16, m8);
+    if constexpr (RTK_USE_TMA && RTK_BIG_PAIR && RTK_TMA_SPLIT && !MASKED && rtk::TmaParts<E>::kSplit &&
+                  MODE != rtk::kTrace) {
+        // paired rows only: one tensor copy per 16 / 8 / 4-float part of each lane row (TmaRow)
+        using P = rtk::TmaParts<E>;
+        const int widths[3] = {P::w0, P::w1, P::w2};
+        CUtensorMap m[3];
+        if (big_pair_eligible<MODE, E>(a) && a.n < (1LL << 31) && rtk_encode_row_parts(m, a.x, a.n, E, a.ldx, widths, P::n))
+            return launch_big_pair_tma_kernel<MODE, E>(a, s, m[0], P::n > 1 ? m[1] : m[0], P::n > 2 ? m[2] : m[0]);
     }
     if constexpr (RTK_USE_TMA && !MASKED && (E == 16 || E == 32)) {
         CUtensorMap map;
@@ -202,7 +208,7 @@ int launch_big(const rtk::Args& a, cudaStream_t s) {
 #define RTK_BIG_PAIR_E32 1
 #endif
             if constexpr (RTK_BIG_PAIR && (E == 16 || (RTK_BIG_PAIR_E32 && E == 32)) && MODE != rtk::kTrace) {
-                if (big_pair_eligible<MODE, E>(a)) return launch_big_pair_tma_kernel<MODE, E>(a, s, map, map);
+                if (big_pair_eligible<MODE, E>(a)) return launch_big_pair_tma_kernel<MODE, E>(a, s, map, map, map);
             }
             if constexpr (MODE == rtk::kTrace) {
                 return launch_big_tma_kernel<MODE, E, true>(a, s, map);
